@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- BinaryAttention forward throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c3|c4|c5a|...]
+
+A "step" is one pass of the hot path (K1 sign-pack+mu, K2 fused attention) over one batch of synthetic
+Q/K/V/bias of the named shape.  Default workload = BASELINE.json configs[1] (DeiT-B attention, B=256 H=12
+N=197 d=64, bf16, dense per-head bias), which fits one GPU.  For N>1 the driver launches this file under
+torchrun: every rank runs the SAME per-GPU batch on its own GPU (weak scaling, heads are independent, no
+collective on the hot path); value = work of all ranks / max-over-ranks device time.
+
+Prints ONE JSON line (see DESIGN.md "Measurement" for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (B, H, N, d, description)
+    "c1": (1, 6, 197, 64, "DeiT-S single forward B=1 H=6 N=197 d=64"),
+    "c2": (256, 12, 197, 64, "DeiT-B attention B=256 H=12 N=197 d=64"),
+    "c3": (64, 16, 256, 72, "DiT-XL/2 256px attention B=64 H=16 N=256 d=72"),
+    "c4": (32, 16, 1024, 72, "DiT-XL/2 512px attention B=32 H=16 N=1024 d=72"),
+    "c5_4096_64": (1, 16, 4096, 64, "high-res sweep B=1 H=16 N=4096 d=64"),
+    "c5_4096_128": (1, 16, 4096, 128, "high-res sweep B=1 H=16 N=4096 d=128"),
+    "c5_8192_128": (1, 16, 8192, 128, "high-res sweep B=1 H=16 N=8192 d=128"),
+    "c5_16384_64": (1, 16, 16384, 64, "high-res sweep B=1 H=16 N=16384 d=64"),
+    "c5_16384_128": (1, 16, 16384, 128, "high-res sweep B=1 H=16 N=16384 d=128"),
+}
+METRIC = "binary_attention_fwd_effective_tops"
+UNIT = "TOPS"  # effective ops = 4*B*H*N^2*d (2*N^2*d for QK^T + 2*N^2*d for P.V), SURVEY.md section 8d
+
+
+def eff_ops(B, H, N, d):
+    return 4.0 * B * H * N * N * d
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"], "bf16_sustained": j["bf16_tflops_sustained"],
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# --------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc = index, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2])); pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # "under load" = samples in the top half of the observed range (idle samples before/after are dropped)
+        hi = [s for s in sm if s >= 0.5 * (min(sm) + max(sm))] or sm
+        return {"sm_mhz": statistics.median(hi), "sm_max_mhz": max(mx), "power_w_max": max(pw), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------------------------- synthetic inputs
+def make_inputs(B, H, N, d, device, seed):
+    """Q,K,V ~ N(0,1) rounded to bf16 (reference bench distribution, bench.cpp:34-39); dense bias N(0,0.5^2)
+    per head shared over the batch (binattn_cli.cpp:49), rows padded to a 16-byte multiple (bias_ld)."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    Q, K, V = (torch.randn(B, H, N, d, device=device, generator=g).to(torch.bfloat16) for _ in range(3))
+    ld = (N + 7) // 8 * 8
+    bias_store = torch.zeros(H, N, ld, device=device, dtype=torch.bfloat16)
+    bias_store[:, :, :N] = (0.5 * torch.randn(H, N, N, device=device, generator=g)).to(torch.bfloat16)
+    return Q, K, V, bias_store[:, :, :N]
+
+
+# --------------------------------------------------------------------------------------------- CPU baseline
+class CpuPath:
+    """The reference's own CPU implementation of the path (oracle/_ref when the reference compiled here, else the
+    C port) on this host's cores, over a bounded sample of heads of the same workload.  quantize_pv=false: the
+    semantics the CUDA path implements (SURVEY.md finding 2).  N <= 256: heads spread over all host threads with
+    one thread per call (intra-call threading does not pay there); N >= 1024: the reference's
+    intra-call parallel_for over query blocks."""
+
+    def __init__(self, B, H, N, d):
+        import numpy as np
+        from oracle import cpu
+        self.np, self.cpu = np, cpu
+        self.lib = cpu.ref() or cpu.port()
+        self.kind = "reference" if self.lib.is_reference else "port"
+        self.cores = os.cpu_count() or 1
+        self.B, self.H, self.N, self.d = B, H, N, d
+        self.small = N <= 256
+        self.quantum = self.cores if self.small else 1
+        self.rng = np.random.default_rng(0)
+        self.data = None
+
+    def prepare(self, heads):
+        N, d = self.N, self.d
+        q, k, v = (self.cpu.bf16_round(self.rng.standard_normal((heads, N, d))) for _ in range(3))
+        bias = self.cpu.bf16_round(0.5 * self.rng.standard_normal((min(heads, self.H), N, N)))
+        self.data = (q, k, v, bias)
+        self.heads = heads
+
+    def run(self):
+        q, k, v, bias = self.data
+        t0 = time.perf_counter()
+        self.lib.binary_attention_fused_heads(q, k, v, bias=bias, quantize_pv=False,
+                                              nthreads=self.cores if self.small else 1,
+                                              intra_threads=1 if self.small else self.cores)
+        return time.perf_counter() - t0
+
+    def calibrate(self, target_s):
+        self.prepare(self.quantum)
+        self.run()                                   # warm-up (page-in, thread spawn)
+        t = self.run()
+        heads = int(min(self.B * self.H, max(1.0, target_s / max(t, 1e-6)) * self.quantum))
+        heads = max(self.quantum, heads // self.quantum * self.quantum)
+        self.prepare(heads)
+        return heads
+
+    def describe(self, times):
+        return (f"{self.heads} of {self.B*self.H} heads (N={self.N}, d={self.d}, dense bias, quantize_pv=false), "
+                f"{'heads over host threads' if self.small else 'intra-call parallel_for'}, {len(times)} timed runs: "
+                f"min/median/max s = {min(times):.3f}/{statistics.median(times):.3f}/{max(times):.3f}")
+
+    def tops(self, seconds):
+        return eff_ops(1, self.heads, self.N, self.d) / seconds / 1e12
+
+
+def cpu_baseline(B, H, N, d, target_s=8.0):
+    c = CpuPath(B, H, N, d)
+    c.calibrate(target_s)
+    times = [c.run() for _ in range(3)]
+    return {"value": c.tops(statistics.median(times)), "unit": UNIT, "cores": c.cores, "kind": c.kind,
+            "sample": c.describe(times)}
+
+
+def run_reference_arm(args, B, H, N, d, rank, world):
+    """--impl reference: K timed steps of the reference CPU path, each step one bounded sample of heads."""
+    if rank != 0:
+        return
+    c = CpuPath(B, H, N, d)
+    c.calibrate(max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup))))
+    for _ in range(args.warmup):
+        c.run()
+    times = [c.run() for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = c.tops(sec)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][4]}", "B_per_gpu": B, "H": H, "N": N,
+                       "d": d, "bias": "dense [H,N,N]",
+                       "note": "reference CPU path on host cores; each step = one bounded sample of heads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": c.cores, "kind": c.kind, "sample": c.describe(times)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------- dense bf16 baseline
+def time_dense_bf16(Q, K, V, bias, steps):
+    """bf16 dense attention on the same GPU (torch SDPA: flash/cuDNN/efficient, whatever wins) -- context only."""
+    import torch
+    import torch.nn.functional as F
+    out = {}
+    for name, mask in (("nobias", None), ("bias", bias.unsqueeze(0) if bias is not None else None)):
+        try:
+            for _ in range(3):
+                F.scaled_dot_product_attention(Q, K, V, attn_mask=mask)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                F.scaled_dot_product_attention(Q, K, V, attn_mask=mask)
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = e0.elapsed_time(e1) / steps
+        except Exception as ex:  # noqa: BLE001
+            out[name] = None
+            out[name + "_error"] = str(ex)[:120]
+    return out
+
+
+# --------------------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--no-bias", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 -> min(steps, 10)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    B, H, N, d, desc = WORKLOADS[args.workload]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, B, H, N, d, rank, world)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_09582_b200 as pkg
+
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device; this benchmark has no CPU fallback"}))
+        return 1
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    ba = pkg.BinaryAttention(device)
+    # weak scaling: every rank owns one full per-GPU batch of independent heads (global heads = world * B * H)
+    Q, K, V, bias = make_inputs(B, H, N, d, device, seed=1234 + rank)
+    if args.no_bias:
+        bias = None
+    kernel = args.kernel
+    used = ba.select_kernel(B, H, N, d, torch.bfloat16, bias) if kernel == "auto" else kernel
+
+    for _ in range(args.warmup):
+        O = ba.forward(Q, K, V, bias, kernel=kernel)
+    barrier()
+
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+        time.sleep(0.25)
+    ba.profile_begin(args.steps)
+    launches0 = ba.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        O = ba.forward(Q, K, V, bias, kernel=kernel)
+    e1.record()
+    barrier()
+    launches = ba.launch_count - launches0
+    total_ms = e0.elapsed_time(e1)
+    calls, pack_ms, attn_ms = ba.profile_end()
+    clocks = sampler.stop() if rank == 0 else None
+
+    t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    value = eff_ops(B, H, N, d) * world / (ms_per_step / 1e3) / 1e12
+
+    # ---- end to end through the host-buffer C-ABI call (H2D + kernels + D2H inside the timed region)
+    e2e_steps = args.e2e_steps or min(args.steps, 10)
+    hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
+    hb = bias.contiguous().cpu().pin_memory() if bias is not None else None
+    hO = torch.empty((B, H, N, d), dtype=torch.float32, pin_memory=True)
+    for _ in range(2):
+        ba.forward_host(hQ, hK, hV, hb, kernel=kernel, out=hO)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ba.forward_host(hQ, hK, hV, hb, kernel=kernel, out=hO)  # synchronises internally; result lands in hO
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    t = torch.tensor([e2e_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = t.item()
+    h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV)) + (hb.numel() * hb.element_size() if hb is not None else 0)
+    d2h = hO.numel() * hO.element_size()
+    e2e_value = eff_ops(B, H, N, d) * world / (e2e_ms / 1e3) / 1e12
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (K2, fused attention): algorithmic bytes / measured launch time
+    pk = peaks()
+    BH = B * H
+    w64 = (d + 63) // 64
+    bias_bytes = (H * N * N * 2) if bias is not None else 0
+    k2_bytes = BH * N * d * (2 + 4) + 2 * BH * N * w64 * 8 + bias_bytes      # V read + O write + packed planes + bias once
+    k1_bytes = BH * N * d * (2 + 2) + 2 * BH * N * w64 * 8                   # Q,K read + packed planes write
+    path_bytes = BH * N * d * (3 * 2 + 4) + bias_bytes                       # SURVEY.md 8d algorithmic bytes
+    pv_flops = 2.0 * BH * N * N * d
+    k2_ms, k1_ms = attn_ms / max(calls, 1), pack_ms / max(calls, 1)
+    t_hbm, t_pv = k2_bytes / (pk["hbm_gbs"] * 1e9), pv_flops / (pk["bf16_sustained"] * 1e12)
+    if t_hbm >= t_pv:
+        achieved = k2_bytes / (k2_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"]}
+    else:
+        achieved = pv_flops / (k2_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_sustained"]}
+    roof.update({"traffic": None, "kernel": f"K2 fused attention ({used})", "kernel_ms": k2_ms,
+                 "algorithmic_bytes": k2_bytes, "peak_source": pk["source"],
+                 "k1_pack": {"ms": k1_ms, "algorithmic_bytes": k1_bytes,
+                             "achieved_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None},
+                 "path": {"algorithmic_bytes": path_bytes, "ms": k1_ms + k2_ms,
+                          "achieved_gbs": path_bytes / ((k1_ms + k2_ms) / 1e3) / 1e9 if k1_ms + k2_ms > 0 else None,
+                          "frac_hbm": path_bytes / ((k1_ms + k2_ms) / 1e3) / 1e9 / pk["hbm_gbs"] if k1_ms + k2_ms > 0 else None},
+                 "mufu_exp_floor_ms": BH * N * N / 4.65e12 * 1e3})
+
+    dense = None if args.no_dense else time_dense_bf16(Q, K, V, bias, min(args.steps, 20))
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(B, H, N, d)
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u1 (sign bits) x e4m3/popc QK^T, bf16 P.V, fp32 softmax/accumulate",
+            "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {desc}", "B_per_gpu": B, "H": H, "N": N, "d": d,
+                       "in_dtype": "bf16", "out_dtype": "fp32", "bias": None if bias is None else "dense [H,N,N] bf16",
+                       "kernel": used, "parallelism": f"heads sharded over {world} GPU(s), no collective",
+                       "l2": "inputs+outputs per step (%.0f MB) exceed the 126 MB L2; no explicit flush" %
+                             (path_bytes / 1e6) if path_bytes > 126e6 else "working set fits L2 (hot-cache number)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "ba_binary_attention_host (pinned host buffers)"},
+            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "dense_bf16_ms": dense,
+            "speedup_vs_dense_bf16": (min(x for x in (dense.get("nobias"), dense.get("bias")) if x) / ms_per_step)
+            if dense and (dense.get("nobias") or dense.get("bias")) else None}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

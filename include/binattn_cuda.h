@@ -1,0 +1,122 @@
+/*
+ * binattn_cuda.h -- C ABI of the B200-native BinaryAttention forward path.
+ *
+ * This is the drop-in boundary around the reference's one hot path
+ *     binattn::binary_attention_fused(q, k, v, cfg)        proj/include/binattn/attention.hpp:69-71
+ * and the L1 functions it calls
+ *     binattn::binary_quantize / pack_signs                proj/src/quantize.cpp:16-23, bitops.cpp:37-49
+ *     binattn::binary_gemm                                 proj/src/bitops.cpp:96-131   (verification only)
+ * mapped to BASELINE.json's operator shape  binary_attention(Q, K, V, bias, scale) -> O:
+ *     Q,K,V  <-> q,k,v  (batched here as [B,H,N,d]; the reference is one call per head)
+ *     bias   <-> cfg.bias after materialize_bias (dense N x N, attention.cpp:55-97), shared over the batch
+ *     scale  <-> 1 / cfg.temperature (default 1/sqrt(d), attention.cpp:49); the data-dependent factor
+ *                mu_q * mu_k (attention.cpp:262-264) is computed INSIDE the call, as in the reference.
+ *     O      <-> AttentionOutput::output;  row_max / row_sum <-> AttentionOutput::row_max / row_sum.
+ *
+ * Conventions: plain C, no exceptions cross the boundary.  Every entry point returns a ba_status;
+ * ba_last_error() gives the thread-local message.  Status codes mirror the reference's exception
+ * types (proj/include/binattn/errors.hpp:10-55): BA_ERR_SHAPE <-> ShapeError, BA_ERR_VALIDATION <->
+ * ValidationError.  All tensor pointers are DEVICE pointers owned by the caller unless the function
+ * name ends in _host.  `stream` is a cudaStream_t passed as void*; calls are asynchronous on it.
+ * One ba_handle per device, used from one host thread at a time.  There is no CPU fallback: without a
+ * CUDA device ba_create fails with BA_ERR_CUDA.
+ */
+#ifndef BINATTN_CUDA_H
+#define BINATTN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BA_OK = 0,
+    BA_ERR_SHAPE = 1,       /* binattn::ShapeError       (errors.hpp:16-19; attention.cpp:21-23, 60-61) */
+    BA_ERR_VALIDATION = 2,  /* binattn::ValidationError  (errors.hpp:22-25; attention.cpp:24-28)        */
+    BA_ERR_CUDA = 3,        /* CUDA runtime / driver failure, or no device                               */
+    BA_ERR_UNSUPPORTED = 4  /* requested kernel cannot run this shape / dtype                            */
+} ba_status;
+
+typedef enum { BA_BF16 = 0, BA_F16 = 1, BA_F32 = 2 } ba_dtype;
+
+typedef enum {
+    BA_KERNEL_AUTO = 0,    /* tcgen05 path when the shape allows it, else the CUDA-core path */
+    BA_KERNEL_SIMT = 1,    /* CUDA-core xor+popc logits, fp32 FMA P.V (any N, d <= 256, any dtype) */
+    BA_KERNEL_TCGEN05 = 2  /* +-1 e4m3 QK^T and bf16 P.V on tcgen05/TMEM, V by TMA (bf16, d % 8 == 0, d <= 128) */
+} ba_kernel;
+
+typedef enum { BA_BIAS_NONE = 0, BA_BIAS_DENSE = 1 } ba_bias_mode;
+
+/* Q, K, V: [B, H, N, d] row-major contiguous, dtype in_dtype.  O: [B, H, N, d] float32.
+ * bias (bias_mode == BA_BIAS_DENSE): [bias_heads, N, bias_ld] with bias_heads in {1, H}; head (b,h)
+ * reads table h % bias_heads; bias_ld >= N is the row stride in elements (0 means N). */
+typedef struct {
+    int32_t B, H, N, d;
+    int32_t in_dtype;    /* ba_dtype of Q, K, V */
+    int32_t bias_mode;   /* ba_bias_mode */
+    int32_t bias_heads;  /* 1 or H */
+    int32_t bias_dtype;  /* BA_BF16 or BA_F32 */
+    int64_t bias_ld;     /* elements; 0 -> N */
+    float inv_tau;       /* 1 / temperature; must be > 0 (attention.cpp:24-25); use 1/sqrt(d) for AttentionConfig::make */
+    int32_t kernel;      /* ba_kernel */
+} ba_params;
+
+typedef struct ba_handle ba_handle;
+
+/* Handle lifetime.  ba_create binds to `device` (cudaSetDevice) and allocates small per-device state. */
+int ba_create(int device, ba_handle** out);
+int ba_destroy(ba_handle* h);
+
+/* Bytes of scratch ba_binary_attention_fwd needs for these params: the packed sign planes of Q and K
+ * ([B,H,N,ceil(d/64)] u64 each, byte-identical to BitMatrix::words(), tensor.hpp:57-94) plus the
+ * per-head mean-abs scales.  Pass workspace = NULL to let the handle own (and cache) it. */
+size_t ba_workspace_bytes(const ba_params* p);
+
+/* binary_quantize (quantize.cpp:16-23) for every head of X [B,H,N,d]:
+ *   words[b,h,i,w]  bit c%64 of word c/64 = 1 iff X[b,h,i,c] >= 0  (pad bits zero; bitops.cpp:37-49)
+ *   mu[b,h]         mean |X[b,h,:,:]| (float32; nullable) */
+int ba_pack_signs(ba_handle* h, const ba_params* p, const void* X, uint64_t* words, float* mu, void* stream);
+
+/* binary_gemm (bitops.cpp:96-131) for ONE head: S[i,j] = d - 2*popc(q_i xor k_j), int32 [N,N].
+ * Verification only (the fused kernel never materialises S). */
+int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, const uint64_t* k_words,
+                     int64_t head_index, int32_t* S, void* stream);
+
+/* binary_attention_fused (attention.cpp:250-382), quantize_pv = false semantics, for all B*H heads.
+ * row_max / row_sum: optional [B,H,N] float32 (AttentionOutput::row_max / row_sum, attention.hpp:45-46). */
+int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
+                            const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
+                            void* stream);
+
+/* Same call with HOST buffers (what a reference-side binding uses): copies Q,K,V(,bias) to the device,
+ * runs ba_binary_attention_fwd, copies O (and row_max/row_sum when non-NULL) back, and synchronises.
+ * Device staging buffers are owned and cached by the handle.  Pinned host memory makes the copies async. */
+int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
+                             const void* bias, float* O, float* row_max, float* row_sum);
+
+/* Launcher partition: contiguous range of the flattened B*H head grid owned by
+ * `rank` of `world` single-GPU processes.  No collective is needed on the hot path. */
+int ba_shard_range(int64_t total_heads, int world, int rank, int64_t* begin, int64_t* end);
+
+/* Which kernel ba_binary_attention_fwd would run for these params (resolves BA_KERNEL_AUTO). */
+int ba_select_kernel(const ba_params* p);
+
+/* Number of CUDA kernels launched through this handle so far (bench.py's gpu_launches). */
+int64_t ba_launch_count(const ba_handle* h);
+
+/* Per-kernel timing for the roofline report.  After ba_profile_begin(h, max_calls) every
+ * ba_binary_attention_fwd call records three CUDA events on ITS launching stream (before K1, between K1
+ * and K2, after K2) until max_calls calls were seen.  ba_profile_end synchronises those events, returns
+ * the number of profiled calls and the summed durations in milliseconds, and switches profiling off. */
+int ba_profile_begin(ba_handle* h, int max_calls);
+int ba_profile_end(ba_handle* h, int* calls, double* pack_ms, double* attn_ms);
+
+const char* ba_last_error(void);
+int ba_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BINATTN_CUDA_H */

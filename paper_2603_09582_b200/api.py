@@ -1,0 +1,293 @@
+"""ctypes binding of include/binattn_cuda.h plus the host-side mirror of the reference's operator API.
+
+Mirrors (names, argument meaning, error behaviour):
+  binattn::AttentionConfig / AttentionConfig::make   proj/include/binattn/attention.hpp:29-41, src/attention.cpp:45-53
+  binattn::AttentionOutput                           attention.hpp:43-48
+  binattn::binary_attention_fused                    attention.hpp:69-71, attention.cpp:250-382
+  binattn::ShapeError / ValidationError              errors.hpp:16-25
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libbinattn_cuda.so")
+
+BA_BF16, BA_F16, BA_F32 = 0, 1, 2
+KERNELS = {"auto": 0, "simt": 1, "tcgen05": 2}
+_DTYPES = {torch.bfloat16: BA_BF16, torch.float16: BA_F16, torch.float32: BA_F32}
+
+
+class BinAttnError(RuntimeError):
+    """binattn::Error (errors.hpp:10-13)."""
+
+
+class ShapeError(BinAttnError):
+    """binattn::ShapeError (errors.hpp:16-19)."""
+
+
+class ValidationError(BinAttnError):
+    """binattn::ValidationError (errors.hpp:22-25)."""
+
+
+class CudaError(BinAttnError):
+    pass
+
+
+class UnsupportedError(BinAttnError):
+    pass
+
+
+_STATUS = {1: ShapeError, 2: ValidationError, 3: CudaError, 4: UnsupportedError}
+
+
+class _Params(C.Structure):
+    _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("N", C.c_int32), ("d", C.c_int32), ("in_dtype", C.c_int32),
+                ("bias_mode", C.c_int32), ("bias_heads", C.c_int32), ("bias_dtype", C.c_int32),
+                ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load libbinattn_cuda.so (built in-tree by paper_2603_09582_b200/build.py).  Fails loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback for this package)")
+    lib = C.CDLL(_LIB_PATH)
+    vp, i64 = C.c_void_p, C.c_int64
+    lib.ba_create.argtypes = [C.c_int, C.POINTER(vp)]
+    lib.ba_destroy.argtypes = [vp]
+    lib.ba_workspace_bytes.argtypes = [C.POINTER(_Params)]
+    lib.ba_workspace_bytes.restype = C.c_size_t
+    lib.ba_pack_signs.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp]
+    lib.ba_binary_logits.argtypes = [vp, C.POINTER(_Params), vp, vp, i64, vp, vp]
+    lib.ba_binary_attention_fwd.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.ba_binary_attention_host.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]
+    lib.ba_shard_range.argtypes = [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
+    lib.ba_select_kernel.argtypes = [C.POINTER(_Params)]
+    lib.ba_launch_count.argtypes = [vp]
+    lib.ba_launch_count.restype = i64
+    lib.ba_profile_begin.argtypes = [vp, C.c_int]
+    lib.ba_profile_end.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.ba_last_error.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc:
+        raise _STATUS.get(rc, BinAttnError)(load_library().ba_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class AttentionConfig:
+    """binattn::AttentionConfig (attention.hpp:29-41).  block_rows/block_cols are accepted and validated like the
+    reference's (attention.cpp:26-28) but do not change the result: the CUDA kernels pick their own tiles and the
+    reference itself is tile-invariant to 1e-12 (test_attention.cpp:254-272).  quantize_pv must be False."""
+    seq_len: int = 0
+    head_dim: int = 0
+    temperature: float = 1.0
+    block_rows: int = 64
+    block_cols: int = 64
+    quantize_pv: bool = False
+    bias: Optional[torch.Tensor] = None  # dense [N,N] (or [Hb,N,N]) table == materialize_bias output
+
+    @staticmethod
+    def make(n: int, d: int) -> "AttentionConfig":  # attention.cpp:45-53
+        return AttentionConfig(seq_len=n, head_dim=d, temperature=math.sqrt(d), block_rows=min(64, n),
+                               block_cols=min(64, n))
+
+
+@dataclass
+class AttentionOutput:
+    """binattn::AttentionOutput (attention.hpp:43-48); probs is never produced by the fused kernels."""
+    output: torch.Tensor
+    row_max: torch.Tensor
+    row_sum: torch.Tensor
+
+
+class BinaryAttention:
+    """One ba_handle bound to one CUDA device."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        self.lib = load_library()
+        if not torch.cuda.is_available():
+            raise CudaError("no CUDA device: paper_2603_09582_b200 has no CPU fallback")
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        h = C.c_void_p()
+        _check(self.lib.ba_create(dev.index, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.ba_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------------------------------
+    def _params(self, B, H, N, d, dtype, bias=None, scale=None, kernel="auto") -> _Params:
+        if dtype not in _DTYPES:
+            raise ValidationError(f"unsupported input dtype {dtype}")
+        p = _Params(B=B, H=H, N=N, d=d, in_dtype=_DTYPES[dtype], kernel=KERNELS[kernel])
+        p.inv_tau = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+        if bias is not None:
+            if bias.dtype not in (torch.bfloat16, torch.float32):
+                raise ValidationError("bias must be bfloat16 or float32")
+            p.bias_mode, p.bias_heads, p.bias_dtype = 1, bias.shape[0], _DTYPES[bias.dtype]
+            p.bias_ld = bias.stride(1)
+        return p
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.ba_launch_count(self.h))
+
+    def profile_begin(self, max_calls: int) -> None:
+        _check(self.lib.ba_profile_begin(self.h, max_calls))
+
+    def profile_end(self):
+        """-> (calls, pack_ms_total, attn_ms_total) from CUDA events recorded on the launching stream."""
+        n, a, b = C.c_int(), C.c_double(), C.c_double()
+        _check(self.lib.ba_profile_end(self.h, C.byref(n), C.byref(a), C.byref(b)))
+        return n.value, a.value, b.value
+
+    def select_kernel(self, B, H, N, d, dtype=torch.bfloat16, bias=None) -> str:
+        p = self._params(B, H, N, d, dtype, bias)
+        k = self.lib.ba_select_kernel(C.byref(p))
+        return {1: "simt", 2: "tcgen05"}.get(k, "none")
+
+    # ------------------------------------------------------------------------------------------
+    def pack_signs(self, X: torch.Tensor):
+        """binary_quantize for every head: returns (words int64 [B,H,N,ceil(d/64)] holding the u64 bit patterns, mu fp32 [B,H])."""
+        if X.dim() != 4:
+            raise ShapeError("pack_signs: X must be [B,H,N,d]")
+        X = X.contiguous()
+        B, H, N, d = X.shape
+        if X.numel() == 0:
+            raise ShapeError("binary_quantize: empty matrix")  # quantize.cpp:17
+        words = torch.empty((B, H, N, (d + 63) // 64), dtype=torch.int64, device=X.device)
+        mu = torch.empty((B, H), dtype=torch.float32, device=X.device)
+        p = self._params(B, H, N, d, X.dtype)
+        _check(self.lib.ba_pack_signs(self.h, C.byref(p), _ptr(X), _ptr(words), _ptr(mu), self._stream()))
+        return words, mu
+
+    def binary_logits(self, q_words: torch.Tensor, k_words: torch.Tensor, d: int, head: int = 0) -> torch.Tensor:
+        """binary_gemm for one head: int32 [N,N] = d - 2*popc(q xor k)."""
+        B, H, N, _ = q_words.shape
+        S = torch.empty((N, N), dtype=torch.int32, device=q_words.device)
+        p = self._params(B, H, N, d, torch.bfloat16)
+        _check(self.lib.ba_binary_logits(self.h, C.byref(p), _ptr(q_words.contiguous()), _ptr(k_words.contiguous()),
+                                         head, _ptr(S), self._stream()))
+        return S
+
+    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False):
+        """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output)."""
+        if Q.dim() != 4:
+            raise ShapeError("attention: Q must be [B,H,N,d]")
+        if K.shape != Q.shape:
+            raise ShapeError("attention: K must be N x d")  # attention.cpp:22
+        if V.shape != Q.shape:
+            raise ShapeError("attention: V must be N x d")  # attention.cpp:23
+        if not (Q.dtype == K.dtype == V.dtype):
+            raise ValidationError("Q, K, V must share one dtype")
+        B, H, N, d = Q.shape
+        Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+        if bias is not None:
+            if bias.dim() == 2:
+                bias = bias.unsqueeze(0)
+            if bias.dim() != 3 or bias.shape[1] != N or bias.shape[2] != N or bias.shape[0] not in (1, H):
+                raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
+            if bias.stride(2) != 1 or bias.stride(0) != bias.stride(1) * N:
+                bias = bias.contiguous()
+        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        O = torch.empty((B, H, N, d), dtype=torch.float32, device=Q.device)
+        m = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
+        l = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
+        _check(self.lib.ba_binary_attention_fwd(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias), _ptr(O),
+                                                _ptr(m), _ptr(l), None, self._stream()))
+        return (O, m, l) if return_stats else O
+
+    def forward_host(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None):
+        """Same call with HOST tensors (ideally pinned): H2D + kernels + D2H inside ba_binary_attention_host."""
+        if Q.is_cuda or K.is_cuda or V.is_cuda:
+            raise ValidationError("forward_host takes CPU tensors")
+        if K.shape != Q.shape or V.shape != Q.shape or Q.dim() != 4:
+            raise ShapeError("attention: Q, K, V must be [B,H,N,d]")
+        B, H, N, d = Q.shape
+        Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+        if bias is not None:
+            bias = (bias.unsqueeze(0) if bias.dim() == 2 else bias).contiguous()
+            if bias.shape[1] != N or bias.shape[2] != N or bias.shape[0] not in (1, H):
+                raise ShapeError("bias: dense table must be N x N")
+        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        if out is None:
+            out = torch.empty((B, H, N, d), dtype=torch.float32, pin_memory=True)
+        _check(self.lib.ba_binary_attention_host(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias), _ptr(out),
+                                                 None, None))
+        return out
+
+
+_handles: dict[int, BinaryAttention] = {}
+
+
+def _handle_for(device: torch.device) -> BinaryAttention:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _handles:
+        _handles[idx] = BinaryAttention(torch.device("cuda", idx))
+    return _handles[idx]
+
+
+def binary_attention(Q, K, V, bias=None, scale=None, kernel="auto"):
+    """BASELINE.json's operator: binary_attention(Q, K, V, bias, scale) -> O.
+
+    Q, K, V: [B,H,N,d] CUDA tensors (bf16 for the tcgen05 kernel; fp16/fp32 run the CUDA-core kernel);
+    bias: None or dense [N,N] / [1|H,N,N] (bf16 or fp32), added before the softmax; scale = 1/temperature
+    (default 1/sqrt(d)).  The per-head factor mu_q*mu_k is computed inside, as in the reference."""
+    if not Q.is_cuda:
+        raise CudaError("binary_attention needs CUDA tensors: this package has no CPU fallback")
+    return _handle_for(Q.device).forward(Q, K, V, bias, scale, kernel)
+
+
+def binary_attention_fused(q, k, v, cfg: AttentionConfig, with_probs: bool = False) -> AttentionOutput:
+    """Drop-in shaped like binattn::binary_attention_fused (attention.hpp:69-71): one head, [N,d] tensors."""
+    n, d = cfg.seq_len, cfg.head_dim
+    for name, t in (("Q", q), ("K", k), ("V", v)):  # attention.cpp:21-23
+        if t.dim() != 2 or t.shape[0] != n or t.shape[1] != d:
+            raise ShapeError(f"attention: {name} must be N x d")
+    if not cfg.temperature > 0.0:  # attention.cpp:24-25
+        raise ValidationError("attention: temperature must be positive")
+    if cfg.block_rows < 1 or cfg.block_rows > n or cfg.block_cols < 1 or cfg.block_cols > n:  # attention.cpp:26-28
+        raise ValidationError("attention: block sizes must be in [1, N]")
+    if cfg.quantize_pv:
+        raise UnsupportedError("quantize_pv=true (int8 P.V) is not built; the CUDA path implements quantize_pv=false")
+    if with_probs:
+        raise UnsupportedError("with_probs is diagnostics-only in the reference and is not carried over")
+    if cfg.bias is not None and (cfg.bias.dim() != 2 or cfg.bias.shape[0] != n or cfg.bias.shape[1] != n):
+        raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
+    ba = _handle_for(q.device)
+    O, m, l = ba.forward(q[None, None], k[None, None], v[None, None], cfg.bias, 1.0 / cfg.temperature,
+                         return_stats=True)
+    return AttentionOutput(O[0, 0], m[0, 0], l[0, 0])

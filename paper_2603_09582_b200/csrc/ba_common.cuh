@@ -1,0 +1,57 @@
+// ba_common.cuh -- shared declarations for the sm_100a BinaryAttention kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "binattn_cuda.h"
+
+namespace ba {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// Device-side view of one forward call (all pointers device pointers).
+struct FwdArgs {
+    const void* V;            // [BH, N, d] in_dtype
+    const uint64_t* q_words;  // [BH, N, W64]
+    const uint64_t* k_words;  // [BH, N, W64]
+    const float* mu_q;        // [BH]
+    const float* mu_k;        // [BH]
+    const void* bias;         // [bias_heads, N, bias_ld] or nullptr
+    float* O;                 // [BH, N, d] fp32
+    float* row_max;           // [BH, N] or nullptr
+    float* row_sum;           // [BH, N] or nullptr
+    int64_t bias_ld;
+    int BH, H, N, d, W64;
+    int bias_heads;
+    int bias_dtype;
+    int in_dtype;
+    float inv_tau;
+};
+
+// Launchers implemented in the .cu files; each returns the number of kernels it launched (>0) or a
+// negative cudaError_t.
+int launch_pack_signs(const void* X, int in_dtype, int64_t heads, int N, int d, uint64_t* words, float* mu,
+                      float* partials, unsigned int* tickets, cudaStream_t stream);
+int pack_partials_per_head(int N, int d, int in_dtype);
+int launch_binary_logits(const uint64_t* qw, const uint64_t* kw, int N, int d, int32_t* S, cudaStream_t stream);
+int launch_attn_simt(const FwdArgs& a, cudaStream_t stream);
+int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
+bool tcgen05_supported(const ba_params* p, const char** why);
+
+__device__ __forceinline__ float to_float(float x) { return x; }
+__device__ __forceinline__ float to_float(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float to_float(__half x) { return __half2float(x); }
+
+__device__ __forceinline__ float load_as_float(const void* base, int dtype, int64_t idx) {
+    if (dtype == BA_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
+    if (dtype == BA_F16) return __half2float(static_cast<const __half*>(base)[idx]);
+    return static_cast<const float*>(base)[idx];
+}
+
+__host__ __device__ inline int dtype_size(int dtype) { return dtype == BA_F32 ? 4 : 2; }
+
+}  // namespace ba

@@ -1,0 +1,238 @@
+// pack_signs.cu -- K1: sign-pack + per-head mean-abs for Q and K (sm_100a).
+//
+// Replaces binattn::binary_quantize = mean|x| + pack_signs
+//   (proj/src/quantize.cpp:16-23, proj/src/bitops.cpp:37-49; layout contract proj/include/binattn/tensor.hpp:57-94):
+//   bit c of row i = 1 iff x[i,c] >= 0 (so +0 and -0 map to +1), LSB-first in u64 words, pad bits zero,
+//   mu = sum|x| / (N*d) per head.
+//
+// HBM-bound streaming kernel: each lane owns one 16-byte vector (8 bf16 / 4 fp32) of a row, builds its
+// 8 (4) sign bits locally, and an 8- (16-) lane shuffle butterfly ORs them into one u64 output word, so
+// every global read is a coalesced 16-byte vector and every write a coalesced 8-byte word.  Rows are padded
+// to whole u64 groups in the LANE mapping only (d=72 -> 9 active + 7 idle lanes per row), never in memory.
+// The per-head |x| sum is reduced block-wide in a fixed order; the last CTA of a head (ticket counter)
+// folds the per-CTA partials in index order, so mu is bit-reproducible run to run.
+#include "ba_common.cuh"
+
+namespace ba {
+
+constexpr int kPackThreads = 256;
+constexpr int kPackRowsPerCta = 256;
+constexpr int kPackUnroll = 4;
+
+struct PackJob {
+    const void* X;
+    uint64_t* words;
+    float* mu;         // [heads] or nullptr
+    float* partials;   // [heads, chunks]
+    unsigned int* tickets;  // [heads], zero on entry, zero on exit
+};
+
+struct PackJobs {
+    PackJob job[2];
+};
+
+__device__ __forceinline__ uint4 ldg_nc_16(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <typename T>
+struct Vec16;
+
+template <>
+struct Vec16<__nv_bfloat16> {
+    static constexpr int kElems = 8;
+    __device__ static void unpack(const uint4& v, float (&f)[8]) {
+        const uint32_t r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            f[2 * i] = __uint_as_float(r[i] << 16);
+            f[2 * i + 1] = __uint_as_float(r[i] & 0xFFFF0000u);
+        }
+    }
+};
+
+template <>
+struct Vec16<__half> {
+    static constexpr int kElems = 8;
+    __device__ static void unpack(const uint4& v, float (&f)[8]) {
+        const uint32_t r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const __half2 h = *reinterpret_cast<const __half2*>(&r[i]);
+            const float2 p = __half22float2(h);
+            f[2 * i] = p.x;
+            f[2 * i + 1] = p.y;
+        }
+    }
+};
+
+template <>
+struct Vec16<float> {
+    static constexpr int kElems = 4;
+    __device__ static void unpack(const uint4& v, float (&f)[4]) {
+        f[0] = __uint_as_float(v.x);
+        f[1] = __uint_as_float(v.y);
+        f[2] = __uint_as_float(v.z);
+        f[3] = __uint_as_float(v.w);
+    }
+};
+
+// Block-wide sum in a fixed order (warp butterfly, then warp 0 over the warp partials); then the
+// last-arriving CTA of the head folds all per-CTA partials in chunk order.
+__device__ __forceinline__ void finish_head_sum(float acc, const PackJob& job, int head, int chunk, int chunks,
+                                               double inv_count) {
+    __shared__ float warp_sums[kPackThreads / 32];
+    __shared__ int is_last;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_sums[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kPackThreads / 32; ++w) s += warp_sums[w];
+        job.partials[(int64_t)head * chunks + chunk] = s;
+        __threadfence();
+        const unsigned int t = atomicAdd(&job.tickets[head], 1u);
+        is_last = (t == (unsigned int)(chunks - 1));
+    }
+    __syncthreads();
+    if (is_last && warp == 0) {
+        __threadfence();
+        double s = 0.0;
+        for (int c = lane; c < chunks; c += 32) s += (double)__ldcg(&job.partials[(int64_t)head * chunks + c]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) {
+            if (job.mu) job.mu[head] = (float)(s * inv_count);
+            job.tickets[head] = 0u;  // self-cleaning for the next call
+        }
+    }
+}
+
+// Fast path: (d * sizeof(T)) % 16 == 0 and X 16-byte aligned.
+template <typename T>
+__global__ void __launch_bounds__(kPackThreads) pack_signs_vec_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int chunks) {
+    constexpr int EPV = Vec16<T>::kElems;  // elements per 16-byte vector
+    constexpr int LPG = 64 / EPV;          // lanes per u64 output word
+    constexpr int HALF = LPG / 2;          // lanes per 32-bit half
+    const PackJob& job = jobs.job[blockIdx.z];
+    const int head = blockIdx.x, chunk = blockIdx.y;
+    const int vpr = d / EPV;                      // vectors per row
+    const int vprp = (vpr + LPG - 1) / LPG * LPG;  // lane slots per row (whole u64 groups)
+    const int w64 = vprp / LPG;
+    const int row0 = chunk * kPackRowsPerCta;
+    const int rows = min(kPackRowsPerCta, N - row0);
+    const int slots = rows * vprp;
+    const int g = threadIdx.x % LPG;  // lane position inside its u64 group (invariant over the loop)
+    const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * (int64_t)sizeof(T);
+    uint64_t* wbase = job.words + ((int64_t)head * N + row0) * w64;
+
+    float acc = 0.f;
+    for (int s0 = 0; s0 < slots; s0 += kPackThreads * kPackUnroll) {
+        uint4 v[kPackUnroll];
+        int rowl[kPackUnroll], vs[kPackUnroll];
+        bool act[kPackUnroll];
+#pragma unroll
+        for (int u = 0; u < kPackUnroll; ++u) {
+            const int s = s0 + u * kPackThreads + threadIdx.x;
+            rowl[u] = s / vprp;
+            vs[u] = s - rowl[u] * vprp;
+            act[u] = (s < slots) && (vs[u] < vpr);
+            v[u] = make_uint4(0, 0, 0, 0);
+            if (act[u]) v[u] = ldg_nc_16(xbase + ((int64_t)rowl[u] * vpr + vs[u]) * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kPackUnroll; ++u) {
+            if (s0 + u * kPackThreads >= slots) break;  // block-uniform
+            float f[EPV];
+            Vec16<T>::unpack(v[u], f);
+            unsigned int m = 0;
+            float sa = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+                m |= (f[e] >= 0.0f ? 1u : 0u) << e;  // -0.0f >= 0 is true, NaN is false: the reference's rule
+                sa += fabsf(f[e]);
+            }
+            if (!act[u]) m = 0;
+            acc += sa;
+            unsigned int w = m << (EPV * (g % HALF));
+#pragma unroll
+            for (int off = 1; off < HALF; off <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, off);
+            const unsigned int hi = __shfl_down_sync(0xffffffffu, w, HALF);
+            if (g == 0 && (s0 + u * kPackThreads + threadIdx.x) < slots)
+                wbase[(int64_t)rowl[u] * w64 + vs[u] / LPG] = ((uint64_t)hi << 32) | (uint64_t)w;
+        }
+    }
+    finish_head_sum(acc, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
+}
+
+// Generic path: any d, any alignment; one thread per (row, u64 word), scalar loads.
+__global__ void __launch_bounds__(kPackThreads) pack_signs_generic_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int dtype,
+                                                                          int chunks) {
+    const PackJob& job = jobs.job[blockIdx.z];
+    const int head = blockIdx.x, chunk = blockIdx.y;
+    const int w64 = (d + 63) / 64;
+    const int row0 = chunk * kPackRowsPerCta;
+    const int rows = min(kPackRowsPerCta, N - row0);
+    float acc = 0.f;
+    for (int s = threadIdx.x; s < rows * w64; s += kPackThreads) {
+        const int rowl = s / w64, w = s - rowl * w64;
+        const int64_t base = ((int64_t)head * N + row0 + rowl) * d;
+        uint64_t bits = 0;
+        const int c1 = min(d, (w + 1) * 64);
+        for (int c = w * 64; c < c1; ++c) {
+            const float x = load_as_float(job.X, dtype, base + c);
+            if (x >= 0.0f) bits |= 1ull << (c & 63);
+            acc += fabsf(x);
+        }
+        job.words[((int64_t)head * N + row0 + rowl) * w64 + w] = bits;
+    }
+    finish_head_sum(acc, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
+}
+
+int pack_partials_per_head(int N, int, int) { return (N + kPackRowsPerCta - 1) / kPackRowsPerCta; }
+
+// Packs one matrix (words/mu) or, when X2 != nullptr via launch_pack_signs2, Q and K in one launch.
+static int launch_pack_jobs(const PackJobs& jobs, int njobs, int in_dtype, int64_t heads, int N, int d,
+                            cudaStream_t stream) {
+    const int chunks = pack_partials_per_head(N, d, in_dtype);
+    const dim3 grid((unsigned)heads, chunks, njobs);
+    const int esz = dtype_size(in_dtype);
+    bool vec = (d * esz) % 16 == 0;
+    for (int j = 0; j < njobs; ++j) vec = vec && (reinterpret_cast<uintptr_t>(jobs.job[j].X) % 16 == 0);
+    if (vec && in_dtype == BA_BF16)
+        pack_signs_vec_kernel<__nv_bfloat16><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
+    else if (vec && in_dtype == BA_F16)
+        pack_signs_vec_kernel<__half><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
+    else if (vec && in_dtype == BA_F32)
+        pack_signs_vec_kernel<float><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
+    else
+        pack_signs_generic_kernel<<<grid, kPackThreads, 0, stream>>>(jobs, N, d, in_dtype, chunks);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+int launch_pack_signs(const void* X, int in_dtype, int64_t heads, int N, int d, uint64_t* words, float* mu,
+                      float* partials, unsigned int* tickets, cudaStream_t stream) {
+    PackJobs jobs{};
+    jobs.job[0] = PackJob{X, words, mu, partials, tickets};
+    return launch_pack_jobs(jobs, 1, in_dtype, heads, N, d, stream);
+}
+
+int launch_pack_signs_qk(const void* Q, const void* K, int in_dtype, int64_t heads, int N, int d, uint64_t* q_words,
+                         uint64_t* k_words, float* mu_q, float* mu_k, float* partials, unsigned int* tickets,
+                         cudaStream_t stream) {
+    const int chunks = pack_partials_per_head(N, d, in_dtype);
+    PackJobs jobs{};
+    jobs.job[0] = PackJob{Q, q_words, mu_q, partials, tickets};
+    jobs.job[1] = PackJob{K, k_words, mu_k, partials + heads * chunks, tickets + heads};
+    return launch_pack_jobs(jobs, 2, in_dtype, heads, N, d, stream);
+}
+
+}  // namespace ba

@@ -1,0 +1,268 @@
+"""Parity tests proper: the CUDA path (through the C ABI) against the CPU oracle on identical inputs.
+
+Bars (BASELINE.json north star): packed sign bits and integer logits BIT-EXACT; O within max-abs 2e-3 of the
+reference's fp64 path (quantize_pv=false); mu within 2e-6 relative.
+Every test runs for each kernel variant the build offers ("simt" always; "tcgen05" when it takes the shape).
+"""
+import numpy as np
+import pytest
+
+from oracle import cpu
+from tests.helpers import make_head_inputs, to_torch, words_to_numpy
+
+pytestmark = pytest.mark.gpu
+
+TOL_O = 2e-3      # max-abs on O vs the fp64 oracle (north star)
+TOL_MU = 2e-6     # relative, fp32 tree sum vs sequential fp64 sum
+
+
+@pytest.fixture(scope="module")
+def ba():
+    import torch
+    import paper_2603_09582_b200 as pkg
+    if not torch.cuda.is_available():
+        pytest.fail("-m gpu tests need a CUDA device")
+    return pkg.BinaryAttention(torch.device("cuda:0"))
+
+
+def kernels_for(ba, B, H, N, d, dtype, bias=None):
+    import torch
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16}[dtype]
+    ks = ["simt"]
+    if ba.select_kernel(B, H, N, d, tdt, bias) == "tcgen05":
+        ks.append("tcgen05")
+    return ks
+
+
+# ------------------------------------------------------------------------------------------ K1 pack + mu
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f16"])
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (33, 5), (3, 130), (50, 12), (1, 1), (700, 200),
+                                 (513, 96)])
+def test_pack_signs_bit_exact(ba, port, n, d, dtype):
+    heads = [make_head_inputs(port, 5, s, n, d, dtype=dtype) for s in range(3)]
+    X = to_torch(np.stack([h[0] for h in heads])[None], dtype)
+    words, mu = ba.pack_signs(X)
+    assert words.shape == (1, 3, n, (d + 63) // 64)
+    for h in range(3):
+        ow, omu = port.binary_quantize(heads[h][0])
+        assert np.array_equal(words_to_numpy(words[0, h]), ow)  # byte-identical to BitMatrix::words()
+        assert abs(float(mu[0, h]) - omu) <= TOL_MU * omu
+
+
+def test_pack_signs_kats(ba, port):
+    import torch
+    # test_bitops.cpp:10-17 (zero -> +1), :19-23 (all negative -> zero words); -0.0 >= 0 (bitops.cpp:45)
+    x = torch.tensor([[[[1.5, -2.0, 0.0]]]], device="cuda", dtype=torch.float32)
+    w, mu = ba.pack_signs(x)
+    assert int(w[0, 0, 0, 0]) == 0b101 and float(mu[0, 0]) == pytest.approx(3.5 / 3)
+    w, _ = ba.pack_signs(-torch.ones(1, 1, 4, 64, device="cuda", dtype=torch.bfloat16))
+    assert not w.any()
+    w, mu = ba.pack_signs(torch.tensor([[[[-0.0, 0.0]]]], device="cuda", dtype=torch.bfloat16))
+    assert int(w[0, 0, 0, 0]) == 0b11 and float(mu[0, 0]) == 0.0  # test_quantize.cpp:16-20
+    up = torch.full((1, 1, 1, 100), 2.0, device="cuda", dtype=torch.bfloat16)  # test_bitops.cpp:55-61
+    wu, _ = ba.pack_signs(up)
+    wd, _ = ba.pack_signs(-up)
+    assert int(wu[0, 0, 0, 0]) == -1 and int(wu[0, 0, 0, 1]) == (1 << 36) - 1 and not wd.any()
+    S = ba.binary_logits(wu, wd, 100)
+    assert int(S[0, 0]) == -100
+    x = torch.tensor([[[[2.0, -2.0], [2.0, -2.0]]]], device="cuda", dtype=torch.float32)  # test_quantize.cpp:9-14
+    assert float(ba.pack_signs(x)[1][0, 0]) == 2.0
+
+
+def test_scale_invariance_of_bits(ba, port):  # test_attention.cpp:330-347
+    q = make_head_inputs(port, 42, 0, 10, 32, dtype="f32")[0]
+    w0, m0 = ba.pack_signs(to_torch(q[None, None], "f32"))
+    w1, m1 = ba.pack_signs(to_torch(7.0 * q[None, None], "f32"))
+    assert (w0 == w1).all() and float(m1) == pytest.approx(7.0 * float(m0), rel=1e-6)
+
+
+def test_pack_is_bit_reproducible(ba, port):
+    X = to_torch(make_head_inputs(port, 9, 0, 2000, 128)[0][None, None], "bf16")
+    w0, m0 = ba.pack_signs(X)
+    for _ in range(3):
+        w1, m1 = ba.pack_signs(X)
+        assert (w0 == w1).all() and (m0 == m1).all()
+
+
+# ------------------------------------------------------------------------------------------ K3 integer logits
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (97, 129), (130, 128), (40, 200)])
+def test_binary_logits_bit_exact(ba, port, n, d):
+    q, k, _, _ = make_head_inputs(port, 17, 1, n, d)
+    qw, _ = ba.pack_signs(to_torch(q[None, None], "bf16"))
+    kw, _ = ba.pack_signs(to_torch(k[None, None], "bf16"))
+    S = ba.binary_logits(qw, kw, d).cpu().numpy()
+    want = port.binary_gemm(port.pack_signs(q), port.pack_signs(k), d)
+    assert np.array_equal(S, want)
+    assert ((S % 2) == d % 2).all() and np.abs(S).max() <= d  # test_bitops.cpp:80-110
+
+
+# ------------------------------------------------------------------------------------------ K2 fused attention
+def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None):
+    """heads: list of (q,k,v,bias) float64; bias_mode in {None,'per_head','shared'}."""
+    import torch
+    H = len(heads)
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], dtype) for i in range(3))
+    bias_t = None
+    if bias_mode == "per_head":
+        bias_t = to_torch(np.stack([h[3] for h in heads]), "bf16")
+    elif bias_mode == "shared":
+        bias_t = to_torch(heads[0][3][None], "bf16")
+    results = {}
+    for kern in kernels_for(ba, 1, H, n, d, dtype, bias_t):
+        O, m, l = ba.forward(Q, K, V, bias_t, scale, kernel=kern, return_stats=True)
+        torch.cuda.synchronize()
+        O, m, l = O.cpu().numpy().astype(np.float64), m.cpu().numpy().astype(np.float64), l.cpu().numpy().astype(np.float64)
+        assert np.isfinite(O).all()
+        for h in range(H):
+            q, k, v, b = heads[h]
+            b = None if bias_mode is None else (heads[0][3] if bias_mode == "shared" else b)
+            tau = None if scale is None else 1.0 / scale
+            y, om, ol = port.binary_attention_fused(q, k, v, tau=tau, bias=b)
+            err = np.abs(O[0, h] - y).max()
+            assert err <= TOL_O, f"{kern}: head {h} max-abs {err:.3e}"
+            # log-sum-exp is tile-invariant: m + ln(l)  (AttentionOutput::row_max/row_sum, attention.hpp:45-46)
+            np.testing.assert_allclose(m[0, h] + np.log(l[0, h]), om + np.log(ol), rtol=0, atol=2e-4)
+        results[kern] = O
+    return results
+
+
+@pytest.mark.parametrize("bias_mode", [None, "per_head", "shared"])
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 64), (129, 64), (300, 72), (48, 16), (33, 8)])
+def test_attention_matches_oracle_bf16(ba, port, n, d, bias_mode):
+    heads = [make_head_inputs(port, 3, s, n, d, bias_scale=0.5) for s in range(3)]
+    run_and_compare(ba, port, heads, n, d, "bf16", bias_mode)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+@pytest.mark.parametrize("n,d", [(50, 12), (33, 5), (7, 16), (100, 100), (64, 129)])
+def test_attention_matches_oracle_other_dtypes(ba, port, n, d, dtype):
+    heads = [make_head_inputs(port, 4, s, n, d, bias_scale=0.4, dtype=dtype) for s in range(2)]
+    run_and_compare(ba, port, heads, n, d, dtype, "per_head")
+
+
+def test_attention_custom_scale_and_d1_fixture(ba, port):
+    import torch
+    # test_attention.cpp:163-174: d=1, N=2, tau=1 -> Y = [3.985164261060192, -1.9851642610601914]
+    q = torch.tensor([[[[2.0], [-1.0]]]], device="cuda")
+    k = torch.tensor([[[[1.0], [-3.0]]]], device="cuda")
+    v = torch.tensor([[[[4.0], [-2.0]]]], device="cuda")
+    O, m, l = ba.forward(q, k, v, None, 1.0, return_stats=True)
+    assert O.flatten().tolist() == pytest.approx([3.985164261060192, -1.9851642610601914], abs=1e-5)
+    assert float(m[0, 0, 0]) == pytest.approx(3.0, abs=1e-5)
+    heads = [make_head_inputs(port, 6, 0, 90, 64, bias_scale=0.5)]
+    run_and_compare(ba, port, heads, 90, 64, "bf16", "per_head", scale=0.05)
+
+
+@pytest.mark.parametrize("case", ["c1_head0", "c1_head5", "c3_head0", "mix_n300_d72", "mix_n130_d128"])
+def test_attention_matches_reference_golden(ba, port, golden, case):
+    """Against outputs of the UNMODIFIED reference (tests/golden, oracle/gen_golden.py)."""
+    import torch
+    c, meta = golden.case(case), golden.meta[case]
+    n, d = meta["n"], meta["d"]
+    q, k, v, bias = make_head_inputs(port, meta["seed"], meta["stream"], n, d, bias_scale=meta["bias_scale"])
+    Q, K, V = (to_torch(x[None, None], "bf16") for x in (q, k, v))
+    B = to_torch(bias[None], "bf16")
+    qw, muq = ba.pack_signs(Q)
+    kw, muk = ba.pack_signs(K)
+    assert np.array_equal(words_to_numpy(qw[0, 0]), c["q_words"]) and np.array_equal(words_to_numpy(kw[0, 0]), c["k_words"])
+    assert abs(float(muq) - c["mu"][0]) <= TOL_MU * c["mu"][0] and abs(float(muk) - c["mu"][1]) <= TOL_MU * c["mu"][1]
+    assert np.array_equal(ba.binary_logits(qw, kw, d).cpu().numpy()[:4], c["logits_rows"])
+    for kern in kernels_for(ba, 1, 1, n, d, "bf16", B):
+        O = ba.forward(Q, K, V, B, kernel=kern)[0, 0].cpu().numpy().astype(np.float64)
+        O_nb = ba.forward(Q, K, V, None, kernel=kern)[0, 0].cpu().numpy().astype(np.float64)
+        assert np.abs(O - c["y"]).max() <= TOL_O and np.abs(O_nb - c["y_nobias"]).max() <= TOL_O
+        # secondary, not gated at 2e-3: distance to the reference's default int8 P.V mode (SURVEY.md finding 2)
+        assert np.abs(O - c["y_int8"]).max() <= 2e-2
+
+
+def test_constant_bias_shift_invariance(ba, port):  # test_attention.cpp:316-328
+    import torch
+    n, d = 120, 64
+    q, k, v, _ = make_head_inputs(port, 41, 0, n, d)
+    Q, K, V = (to_torch(x[None, None], "bf16") for x in (q, k, v))
+    shift = torch.full((1, n, n), -1.75, device="cuda", dtype=torch.float32)
+    for kern in kernels_for(ba, 1, 1, n, d, "bf16"):
+        y0 = ba.forward(Q, K, V, None, kernel=kern)
+        y1 = ba.forward(Q, K, V, shift, kernel=kern)
+        assert (y0 - y1).abs().max().item() <= 1e-5
+
+
+def test_bias_row_stride(ba, port):
+    """bias_ld > N (padded rows) gives the same result as the dense N x N table."""
+    import torch
+    n, d = 197, 64
+    q, k, v, bias = make_head_inputs(port, 8, 0, n, d, bias_scale=0.5)
+    Q, K, V = (to_torch(x[None, None], "bf16") for x in (q, k, v))
+    dense = to_torch(bias[None], "bf16")
+    padded = torch.zeros(1, n, 200, device="cuda", dtype=torch.bfloat16)
+    padded[:, :, :n] = dense
+    for kern in kernels_for(ba, 1, 1, n, d, "bf16", dense):
+        y0 = ba.forward(Q, K, V, dense, kernel=kern)
+        y1 = ba.forward(Q, K, V, padded[:, :, :n], kernel=kern)
+        assert torch.equal(y0, y1)
+
+
+def test_run_to_run_and_shard_identity(ba, port):
+    """Determinism + SURVEY.md 8e: running a sub-range of heads gives byte-identical rows to the full run."""
+    import torch
+    from paper_2603_09582_b200 import shard_range
+    B, H, n, d = 2, 4, 197, 64
+    heads = [make_head_inputs(port, 12, s, n, d, bias_scale=0.5) for s in range(B * H)]
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads]).reshape(B, H, n, d), "bf16") for i in range(3))
+    for kern in kernels_for(ba, B, H, n, d, "bf16"):
+        full = ba.forward(Q, K, V, None, kernel=kern)
+        assert torch.equal(full, ba.forward(Q, K, V, None, kernel=kern))
+        for world in (2, 3):
+            parts = []
+            for rank in range(world):
+                b, e = shard_range(B * H, world, rank)
+                sl = lambda t: t.reshape(1, B * H, n, d)[:, b:e].contiguous()
+                parts.append(ba.forward(sl(Q), sl(K), sl(V), None, kernel=kern))
+            assert torch.equal(torch.cat(parts, dim=1).reshape(B, H, n, d), full)
+
+
+def test_host_buffer_entry_point(ba, port):
+    import torch
+    n, d = 197, 64
+    heads = [make_head_inputs(port, 13, s, n, d, bias_scale=0.5) for s in range(4)]
+    Qh, Kh, Vh = (to_torch(np.stack([h[i] for h in heads])[None], "bf16", "cpu").pin_memory() for i in range(3))
+    bh = to_torch(np.stack([h[3] for h in heads]), "bf16", "cpu").pin_memory()
+    out = ba.forward_host(Qh, Kh, Vh, bh)
+    dev = ba.forward(Qh.cuda(), Kh.cuda(), Vh.cuda(), bh.cuda())
+    assert torch.equal(out, dev.cpu())
+
+
+def test_error_codes_on_device(ba):
+    import torch
+    import paper_2603_09582_b200 as pkg
+    q = torch.zeros(1, 1, 4, 8, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(pkg.ShapeError):
+        ba.forward(q, q[:, :, :, :4], q)
+    with pytest.raises(pkg.ValidationError):  # attention.cpp:24-25
+        ba.forward(q, q, q, None, 0.0)
+    with pytest.raises(pkg.ShapeError):  # attention.cpp:60-61
+        ba.forward(q, q, q, torch.zeros(1, 3, 3, device="cuda"))
+    with pytest.raises(pkg.ShapeError):  # quantize.cpp:17
+        ba.pack_signs(torch.zeros(1, 1, 0, 8, device="cuda"))
+
+
+def test_full_size_c2_properties(ba, port):
+    """BASELINE.json configs[1] (DeiT-B, B=256 H=12 N=197 d=64) at full size: sampled heads against the oracle,
+    plus size-independent properties (key-permutation invariance, rows of P sum to one via V = 1)."""
+    import torch
+    B, H, n, d = 256, 12, 197, 64
+    g = torch.Generator(device="cuda").manual_seed(0)
+    Q, K, V = (torch.randn(B, H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    bias = (0.5 * torch.randn(H, n, n, device="cuda", generator=g)).to(torch.bfloat16)
+    for kern in kernels_for(ba, B, H, n, d, "bf16", bias):
+        O = ba.forward(Q, K, V, bias, kernel=kern)
+        assert torch.isfinite(O).all()
+        for (b, h) in [(0, 0), (17, 5), (255, 11)]:
+            f = lambda t: t[b, h].float().cpu().numpy().astype(np.float64)
+            y = port.binary_attention_fused(f(Q), f(K), f(V), bias=bias[h].float().cpu().numpy().astype(np.float64))[0]
+            assert np.abs(O[b, h].cpu().numpy() - y).max() <= TOL_O
+        ones = ba.forward(Q[:8], K[:8], torch.ones_like(V[:8]), bias, kernel=kern)
+        assert (ones - 1.0).abs().max().item() <= 1e-3  # softmax rows sum to one
+        perm = torch.randperm(n, device="cuda", generator=g)
+        Op = ba.forward(Q[:8], K[:8, :, perm], V[:8, :, perm], bias[:, :, perm], kernel=kern)
+        assert (Op - O[:8]).abs().max().item() <= 1e-3  # attention is a set function of (k_j, v_j, b_ij)
