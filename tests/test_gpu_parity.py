@@ -103,10 +103,11 @@ def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None):
     H = len(heads)
     Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], dtype) for i in range(3))
     bias_t = None
+    bdt = "bf16" if dtype == "bf16" else "f32"  # bias values were rounded to `dtype`; f16 values are exact in f32
     if bias_mode == "per_head":
-        bias_t = to_torch(np.stack([h[3] for h in heads]), "bf16")
+        bias_t = to_torch(np.stack([h[3] for h in heads]), bdt)
     elif bias_mode == "shared":
-        bias_t = to_torch(heads[0][3][None], "bf16")
+        bias_t = to_torch(heads[0][3][None], bdt)
     results = {}
     for kern in kernels_for(ba, 1, H, n, d, dtype, bias_t):
         O, m, l = ba.forward(Q, K, V, bias_t, scale, kernel=kern, return_stats=True)
@@ -266,3 +267,25 @@ def test_full_size_c2_properties(ba, port):
         perm = torch.randperm(n, device="cuda", generator=g)
         Op = ba.forward(Q[:8], K[:8, :, perm], V[:8, :, perm], bias[:, :, perm], kernel=kern)
         assert (Op - O[:8]).abs().max().item() <= 1e-3  # attention is a set function of (k_j, v_j, b_ij)
+
+
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 32), (300, 96)])
+def test_tensor_core_logits_bit_exact(ba, port, n, d):
+    """The e4m3 +-1 tcgen05 contraction inside the fused kernel reproduces the integer logits exactly
+    (debug dump of the TMEM accumulators; BASELINE.json: 'integer QK^T logits must be bit-exact')."""
+    import ctypes as C
+    import torch
+    if ba.select_kernel(1, 2, n, d, torch.bfloat16) != "tcgen05":
+        pytest.skip("tcgen05 kernel does not take this shape")
+    heads = [make_head_inputs(port, 21, s, n, d) for s in range(2)]
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
+    S = torch.full((n, n), -12345, dtype=torch.int32, device="cuda")
+    ba.lib.ba_debug_tcgen05_logits.argtypes = [C.c_void_p, C.c_int]
+    ba.lib.ba_debug_tcgen05_logits(C.c_void_p(S.data_ptr()), 1)
+    try:
+        ba.forward(Q, K, V, None, kernel="tcgen05")
+        torch.cuda.synchronize()
+    finally:
+        ba.lib.ba_debug_tcgen05_logits(None, -1)
+    want = port.binary_gemm(port.pack_signs(heads[1][0]), port.pack_signs(heads[1][1]), d)
+    assert np.array_equal(S.cpu().numpy(), want)
