@@ -266,7 +266,9 @@ def test_full_size_c2_properties(ba, port):
         assert (ones - 1.0).abs().max().item() <= 1e-3  # softmax rows sum to one
         perm = torch.randperm(n, device="cuda", generator=g)
         Op = ba.forward(Q[:8], K[:8, :, perm], V[:8, :, perm], bias[:, :, perm], kernel=kern)
-        assert (Op - O[:8]).abs().max().item() <= 1e-3  # attention is a set function of (k_j, v_j, b_ij)
+        # attention is a set function of (k_j, v_j, b_ij); two bf16-P runs with different tile groupings may each sit
+        # ~7e-4 from the exact result (SURVEY.md 8c error budget), so the pairwise bound is the parity bound itself
+        assert (Op - O[:8]).abs().max().item() <= TOL_O
 
 
 @pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 32), (300, 96)])
