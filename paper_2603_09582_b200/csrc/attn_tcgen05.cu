@@ -16,7 +16,8 @@
 //   warp  4    TMEM allocation + single-thread tcgen05.mma issue
 //   warp  5    TMA producer for V
 //   warps 6-7  K-tile expanders (bit plane -> e4m3 bytes, one key per thread)
-// Pipelines (mbarriers): K bytes 2 stages, V 2 stages, S (TMEM) 2 stages, P (smem) 2 stages.  The running max uses
+// Pipelines (mbarriers): K bytes 2 stages, V 2 stages, S (TMEM) 2 stages, P (smem) 1-2 stages, bias tile (bf16,
+// TMA, 128B swizzle) 1-2 stages -- the stage counts are picked on the host so that two CTAs fit one SM.  The running max uses
 // the lazy-rescale rule: O/l are rescaled only when a row max grows by more than 2^8, which keeps TMEM read-modify-
 // write traffic off the common path; the final O/l is unaffected (both carry the same reference max).
 #include <cuda.h>
@@ -32,7 +33,8 @@ constexpr int kThreads = 256;
 constexpr int kTmemCols = 256;   // S0 [0,64) | S1 [64,128) | O [128, 128+DVP)
 constexpr int kColS = 0, kColO = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr uint32_t kSpinLimit = 1u << 24;
+constexpr uint64_t kHangNs = 4000000000ull;
+constexpr uint32_t kSuspendHint = 0x989680;  // try_wait may sleep this long before re-polling (cuts spin instructions)
 
 // ------------------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -46,20 +48,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// Bounded spin: a protocol bug traps (clean launch failure) instead of hanging the GPU.
+// Bounded wait: a protocol bug traps after ~4 s (clean launch failure) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0, spins = 0;
+    uint32_t done = 0;
+    uint64_t t0 = 0;
     while (true) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(addr), "r"(parity)
+            : "r"(addr), "r"(parity), "r"(kSuspendHint)
             : "memory");
         if (done) break;
-        if (++spins > kSpinLimit) __trap();
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kHangNs) __trap();
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -129,23 +135,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
-// 4 sign bits (bit = 1 -> +1.0) -> 4 e4m3 bytes: +1.0 = 0x38, -1.0 = 0xB8.
-__device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
-    return 0xB8B8B8B8u ^ ((nib * 0x10204080u) & 0x80808080u);
-}
-// 16 sign bits starting at element e0 of a row of logical width d -> 16 bytes (elements >= d become 0.0).
-__device__ __forceinline__ uint4 expand16(uint32_t bits16, int e0, int d) {
-    uint4 v;
-    v.x = (e0 + 0 < d) ? expand_nibble(bits16 & 0xF) : 0u;
-    v.y = (e0 + 4 < d) ? expand_nibble((bits16 >> 4) & 0xF) : 0u;
-    v.z = (e0 + 8 < d) ? expand_nibble((bits16 >> 8) & 0xF) : 0u;
-    v.w = (e0 + 12 < d) ? expand_nibble((bits16 >> 12) & 0xF) : 0u;
+// 8 sign bits (bit = 1 -> +1.0) -> 8 e4m3 bytes: +1.0 = 0x38, -1.0 = 0xB8.  Used once per CTA to build the
+// 256-entry lookup table the expanders read (one 8-byte shared-memory load per 8 elements).
+__device__ __forceinline__ uint2 expand_byte(uint32_t b) {
+    uint2 v;
+    v.x = 0xB8B8B8B8u ^ (((b & 0xF) * 0x10204080u) & 0x80808080u);
+    v.y = 0xB8B8B8B8u ^ ((((b >> 4) & 0xF) * 0x10204080u) & 0x80808080u);
     return v;
 }
 
 struct Smem {
-    // barriers first (8-byte aligned), tiles after (1024-byte aligned for the swizzled V stages)
-    uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], sempty[2], pfull[2], pempty[2];
+    uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], sempty[2], pfull[2], pempty[2], bfull[2], bempty[2];
+    uint2 lut[256];  // byte of sign bits -> 8 e4m3 +-1.0 bytes
     uint32_t tmem_base;
 };
 
@@ -155,52 +156,112 @@ struct Params {
     int tiles;         // ceil(N / BN)
     int dvp;           // d rounded up to 16 (UMMA N of P.V)
     int nbox;          // ceil(d / 64) TMA boxes per V tile
+    int pstages;       // P stages in shared memory (1 or 2)
+    int bstages;       // bias-tile stages (0 = no TMA bias, 1 or 2)
+    int rowsum_mma;    // 1: the softmax denominator is column dvp of the P.V MMA (V tile extended by a block of ones)
     int32_t* dbg_S;    // optional [N,N] int32 dump of the logits of head dbg_head (tests only)
     int dbg_head;
+    long long* dbg_T;  // optional timeline: [cta][role 0..3][128] clock64 stamps (dev tool, TL kernels only)
 };
 
-// Expand row `row` (packed u64 words, or zeros when !valid) into a K-major no-swizzle e4m3 tile:
-// byte (r, kb) lives at (kb/16) * (rows*16) + r*16 + kb%16   (8x16B core matrices, SBO = 128, LBO = rows*16).
+// Packed sign words of one row -> KPAD/32 32-bit registers (zeros when !valid).
 template <int KPAD>
-__device__ __forceinline__ void expand_row(unsigned char* tile, int rows, int r, const uint64_t* words, int w64, int d,
-                                           bool valid) {
-    uint32_t w32[KPAD / 32];
+__device__ __forceinline__ void load_words(uint32_t (&w32)[KPAD / 32], const uint64_t* words, int w64, bool valid) {
 #pragma unroll
-    for (int i = 0; i < KPAD / 64; ++i) {
+    for (int i = 0; i < (KPAD + 63) / 64; ++i) {
         const uint64_t w = (valid && i < w64) ? __ldg(words + i) : 0ull;
         w32[2 * i] = (uint32_t)w;
-        w32[2 * i + 1] = (uint32_t)(w >> 32);
-    }
-    if constexpr (KPAD % 64 != 0) {  // KPAD = 32 or 96: one extra 32-bit half word
-        const int i = KPAD / 64;
-        const uint64_t w = (valid && i < w64) ? __ldg(words + i) : 0ull;
-        w32[KPAD / 32 - 1] = (uint32_t)w;
-    }
-#pragma unroll
-    for (int c = 0; c < KPAD / 16; ++c) {
-        const uint32_t bits16 = (w32[c / 2] >> (16 * (c & 1))) & 0xFFFFu;
-        const uint4 v = valid ? expand16(bits16, 16 * c, d) : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(tile + (size_t)c * rows * 16 + r * 16) = v;
+        if (2 * i + 1 < KPAD / 32) w32[2 * i + 1] = (uint32_t)(w >> 32);
     }
 }
 
+// Expand one row into a K-major no-swizzle e4m3 tile through the lookup table:
+// byte (r, kb) lives at (kb/16) * (rows*16) + r*16 + kb%16   (8x16B core matrices, SBO = 128, LBO = rows*16).
+// d % 8 == 0, so validity is decided per 8-element group; groups at or past d (and whole invalid rows) store 0.0.
 template <int KPAD>
+__device__ __forceinline__ void expand_store(unsigned char* tile, int rows, int r, const uint32_t (&w32)[KPAD / 32],
+                                             int d, bool valid, const uint2* lut) {
+#pragma unroll
+    for (int c = 0; c < KPAD / 16; ++c) {
+        const uint32_t bits16 = w32[c / 2] >> (16 * (c & 1));
+        const uint2 lo = (valid && 16 * c < d) ? lut[bits16 & 0xFF] : make_uint2(0, 0);
+        const uint2 hi = (valid && 16 * c + 8 < d) ? lut[(bits16 >> 8) & 0xFF] : make_uint2(0, 0);
+        *reinterpret_cast<uint4*>(tile + (size_t)c * rows * 16 + r * 16) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+    }
+}
+
+// Row maximum of one 64-column score tile (4 independent chains); MASKED ignores columns >= nk.
+template <bool MASKED>
+__device__ __forceinline__ float tile_max(const float (&x)[BN], int nk) {
+    float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < BN; i += 4) {
+        m0 = fmaxf(m0, (!MASKED || i + 0 < nk) ? x[i + 0] : -INFINITY);
+        m1 = fmaxf(m1, (!MASKED || i + 1 < nk) ? x[i + 1] : -INFINITY);
+        m2 = fmaxf(m2, (!MASKED || i + 2 < nk) ? x[i + 2] : -INFINITY);
+        m3 = fmaxf(m3, (!MASKED || i + 3 < nk) ? x[i + 3] : -INFINITY);
+    }
+    return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+}
+
+// p = 2^(x*ea - m_ref) packed to bf16 pairs; SUM adds the fp32 row sum (otherwise the tensor core sums the
+// bf16 values through the ones block).  MASKED zeroes columns >= nk.
+template <bool MASKED, bool SUM>
+__device__ __forceinline__ float exp_pack(const float (&x)[BN], int nk, float ea, float nm, uint32_t (&pk)[BN / 2]) {
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < BN; i += 2) {
+        float p0 = ex2(fmaf(x[i], ea, nm));
+        float p1 = ex2(fmaf(x[i + 1], ea, nm));
+        if (MASKED) {
+            p0 = (i < nk) ? p0 : 0.f;
+            p1 = (i + 1 < nk) ? p1 : 0.f;
+        }
+        if (SUM) {
+            l0 += p0;
+            l1 += p1;
+        }
+        pk[i / 2] = pack_bf16(p0, p1);
+    }
+    return l0 + l1;
+}
+
+// BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
+#define BA_STAMP(role)                                                                  \
+    do {                                                                                \
+        if (TL && tl_buf && tl_n < 128) tl_buf[(role) * 128 + tl_n++] = clock64();      \
+    } while (0)
+
+template <int KPAD, int BIAS, bool TL = false>
 __global__ void __launch_bounds__(kThreads, 2)
-attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap) {
+attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap,
+               const __grid_constant__ CUtensorMap bmap) {
+    // d <= 96 leaves 16 spare TMEM columns next to O: the softmax denominator is then accumulated by the tensor
+    // core (P x ones), which removes one FADD per score from the softmax warps.
+    constexpr bool ROWSUM = KPAD <= 96;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
-    // carve shared memory: V stages (1024-aligned) | P stages | Q tile | K stages | barriers
+    // carve shared memory: V stages | bias stages (both 1024-aligned, swizzled) | P stages | Q tile | K stages | ones | barriers
     unsigned char* sV = smem_raw;                                   // 2 x nbox x 8192
-    unsigned char* sP = sV + 2 * prm.nbox * 8192;                   // 2 x 16384
-    unsigned char* sQ = sP + 2 * 16384;                             // BM x KPAD
+    unsigned char* sB = sV + 2 * prm.nbox * 8192;                   // bstages x 16384
+    unsigned char* sP = sB + prm.bstages * 16384;                   // pstages x 16384
+    unsigned char* sQ = sP + prm.pstages * 16384;                   // BM x KPAD
     unsigned char* sK = sQ + BM * KPAD;                             // 2 x BN x KPAD
-    Smem* sm = reinterpret_cast<Smem*>(sK + 2 * BN * KPAD);
+    unsigned char* sOnes = sK + 2 * BN * KPAD;                      // 512 B of bf16 1.0 (B operand of the row-sum MMA)
+    Smem* sm = reinterpret_cast<Smem*>(sOnes + 512);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int head = blockIdx.x / prm.mblocks;
     const int mb = blockIdx.x - head * prm.mblocks;
     const int N = a.N, d = a.d, w64 = a.W64, T = prm.tiles;
     const int row0 = mb * BM;
+    const bool p2 = prm.pstages == 2, b2 = prm.bstages == 2;
+    const int ocols = prm.dvp + (ROWSUM ? 16 : 0);  // TMEM columns of the O accumulator (+ denominator block)
+    long long* tl_buf = (TL && prm.dbg_T) ? prm.dbg_T + (size_t)blockIdx.x * 4 * 128 : nullptr;
+    int tl_n = 0;
+    (void)tl_buf; (void)tl_n;
+    if (TL && !(tid == 0 || tid == 128 || tid == 160 || tid == 192)) tl_buf = nullptr;  // one stamper per role
+    BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
 
     // ---------------------------------------------------------------- prologue
     if (tid == 0) {
@@ -213,6 +274,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             mbar_init(&sm->sempty[s], 128); // every softmax thread arrives
             mbar_init(&sm->pfull[s], 128);  // every softmax thread arrives
             mbar_init(&sm->pempty[s], 1);   // tcgen05.commit
+            mbar_init(&sm->bfull[s], 1);    // expect_tx arrive + TMA bytes
+            mbar_init(&sm->bempty[s], 128); // every softmax thread arrives
         }
         fence_barrier_init();
     }
@@ -222,17 +285,24 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (warp == 5 && lane == 0)
+    if (warp == 5 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
-    if (tid < BM) {  // Q tile: thread r expands query row row0 + r (zeros past N)
-        const int row = row0 + tid;
-        expand_row<KPAD>(sQ, BM, tid, a.q_words + ((int64_t)head * N + row) * w64, w64, d, row < N);
+        if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
     }
+    sm->lut[tid] = expand_byte((uint32_t)tid);
+    if (tid < 128) reinterpret_cast<uint32_t*>(sOnes)[tid] = 0x3F803F80u;  // bf16 1.0 pairs
+    // the first packed words are fetched before the barrier so their latency overlaps the table build
+    uint32_t w32[KPAD / 32];
+    if (tid < BM) load_words<KPAD>(w32, a.q_words + ((int64_t)head * N + row0 + tid) * w64, w64, row0 + tid < N);
+    else if (warp >= 6) load_words<KPAD>(w32, a.k_words + ((int64_t)head * N + (tid - 192)) * w64, w64, tid - 192 < N);
+    __syncthreads();
+    if (tid < BM) expand_store<KPAD>(sQ, BM, tid, w32, d, row0 + tid < N, sm->lut);  // Q tile: thread r = query row
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm->tmem_base;
+    BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
 
     if (warp == 4) {
         // ============================================================ MMA issuer
@@ -241,28 +311,39 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             const uint32_t idesc_s = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);  // e4m3 x e4m3 -> f32, K-major A/B
             const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |                      // bf16 x bf16 -> f32, B MN-major
                                       ((uint32_t)(prm.dvp >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc_l = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) |      // bf16 x ones(K-major) -> f32, N = 16
+                                     ((uint32_t)(BM >> 4) << 24);
             const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), p_addr = smem_u32(sP), v_addr = smem_u32(sV);
+            const uint64_t ones_desc = make_desc(smem_u32(sOnes), 256, 128, 0);  // 16 x 16 block of ones, any layout reads 1.0
             auto issue_pv = [&](int t) {
                 const int s = t & 1, n = t >> 1;
-                mbar_wait(&sm->pfull[s], n & 1);
+                const int ps = p2 ? s : 0, pn = p2 ? n : t;
+                mbar_wait(&sm->pfull[ps], pn & 1);
+                BA_STAMP(1);
                 mbar_wait(&sm->vfull[s], n & 1);
+                BA_STAMP(1);
                 tc_fence_after();
                 const int nk = min(BN, N - t * BN);
                 const int ksteps = (nk + 15) >> 4;
                 for (int ks = 0; ks < ksteps; ++ks) {
                     // A = P (K-major, no swizzle): 16 bf16 per step = 2 core-matrix columns of 2048 B
-                    const uint64_t ad = make_desc(p_addr + s * 16384 + ks * 4096, 2048, 128, 0);
+                    const uint64_t ad = make_desc(p_addr + ps * 16384 + ks * 4096, 2048, 128, 0);
                     // B = V tile (MN-major, 128B swizzle): 16 keys per step = 2048 B; next 64 columns = next TMA box
                     const uint64_t bd = make_desc(v_addr + s * prm.nbox * 8192 + ks * 2048, 8192, 1024, 2);
-                    mma_bf16(tmem + kColO, ad, bd, idesc_pv, (t > 0 || ks > 0) ? 1u : 0u);
+                    const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
+                    mma_bf16(tmem + kColO, ad, bd, idesc_pv, acc);
+                    if (ROWSUM) mma_bf16(tmem + kColO + prm.dvp, ad, ones_desc, idesc_l, acc);
                 }
-                tc_commit(&sm->pempty[s]);
+                tc_commit(&sm->pempty[ps]);
                 tc_commit(&sm->vempty[s]);
+                BA_STAMP(1);
             };
             for (int j = 0; j < T; ++j) {
                 const int s = j & 1, n = j >> 1;
                 mbar_wait(&sm->kfull[s], n & 1);
+                BA_STAMP(1);
                 mbar_wait(&sm->sempty[s], (n & 1) ^ 1);
+                BA_STAMP(1);
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < KPAD / 32; ++ks) {
@@ -272,16 +353,26 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 }
                 tc_commit(&sm->sfull[s]);
                 tc_commit(&sm->kempty[s]);
+                BA_STAMP(1);
                 if (j > 0) issue_pv(j - 1);
             }
             issue_pv(T - 1);
         }
     } else if (warp == 5) {
-        // ============================================================ TMA producer (V tiles)
+        // ============================================================ TMA producer (V tiles, bias tiles)
         if (lane == 0) {
+            const int bh = head % a.H % a.bias_heads;
             for (int j = 0; j < T; ++j) {
                 const int s = j & 1, n = j >> 1;
+                if (BIAS == 1) {
+                    const int bs = b2 ? s : 0, bn = b2 ? n : j;
+                    mbar_wait(&sm->bempty[bs], (bn & 1) ^ 1);
+                    mbar_expect_tx(&sm->bfull[bs], 16384);
+                    tma_load_3d(&bmap, &sm->bfull[bs], sB + bs * 16384, j * BN, row0, bh);
+                }
+                BA_STAMP(2);
                 mbar_wait(&sm->vempty[s], (n & 1) ^ 1);
+                BA_STAMP(2);
                 mbar_expect_tx(&sm->vfull[s], prm.nbox * 8192);
                 for (int b = 0; b < prm.nbox; ++b)
                     tma_load_3d(&vmap, &sm->vfull[s], sV + (s * prm.nbox + b) * 8192, b * 64, j * BN, head);
@@ -292,30 +383,51 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         const int t = tid - 6 * 32;
         for (int j = 0; j < T; ++j) {
             const int s = j & 1, n = j >> 1;
-            mbar_wait(&sm->kempty[s], (n & 1) ^ 1);
             const int key = j * BN + t;
-            expand_row<KPAD>(sK + s * BN * KPAD, BN, t, a.k_words + ((int64_t)head * N + key) * w64, w64, d, key < N);
+            mbar_wait(&sm->kempty[s], (n & 1) ^ 1);
+            BA_STAMP(3);
+            expand_store<KPAD>(sK + s * BN * KPAD, BN, t, w32, d, key < N, sm->lut);
+            BA_STAMP(3);
             fence_proxy_async();
             mbar_arrive(&sm->kfull[s]);
+            BA_STAMP(3);
+            // prefetch the next tile's words so their L2 latency hides behind the next wait
+            if (j + 1 < T) load_words<KPAD>(w32, a.k_words + ((int64_t)head * N + key + BN) * w64, w64, key + BN < N);
         }
     } else {
         // ============================================================ softmax + epilogue (thread = query row)
         const int row = row0 + tid;
         const bool row_ok = row < N;
+        const bool warp_ok = row0 + warp * 32 < N;  // warps whose 32 rows are all past N only keep the barriers moving
         const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-        const float sc2 = a.mu_q[head] * a.mu_k[head] * a.inv_tau * kLog2e;
+        const float sc = a.mu_q[head] * a.mu_k[head] * a.inv_tau;  // natural-log units per unit of dot
+        // BIAS == 0 keeps x = raw integer dot and folds sc*log2e into the exponent FMA; otherwise x = dot*sc + bias
+        const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;
         const char* bias_row = nullptr;
-        const int bsz = dtype_size(a.bias_dtype);
-        if (a.bias && row_ok)
-            bias_row = static_cast<const char*>(a.bias) + ((int64_t)(head % a.H % a.bias_heads) * N + row) * a.bias_ld * bsz;
-        const bool bias_vec = bias_row && a.bias_dtype == BA_BF16 && (reinterpret_cast<uintptr_t>(bias_row) % 16 == 0);
-        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.f;
+        if (BIAS == 2 && row_ok)
+            bias_row = static_cast<const char*>(a.bias) +
+                       ((int64_t)(head % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.f;  // base-2 units
 
         for (int j = 0; j < T; ++j) {
             const int s = j & 1, n = j >> 1;
+            const int ps = p2 ? s : 0, pn = p2 ? n : j;
+            const int bs = b2 ? s : 0, bn = b2 ? n : j;
             const int nk = min(BN, N - j * BN);
-            float x[BN];
+            BA_STAMP(0);
             mbar_wait(&sm->sfull[s], n & 1);
+            BA_STAMP(0);
+            if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
+                mbar_arrive(&sm->sempty[s]);
+                if (BIAS == 1) {
+                    mbar_wait(&sm->bfull[bs], bn & 1);
+                    mbar_arrive(&sm->bempty[bs]);
+                }
+                mbar_wait(&sm->pempty[ps], (pn & 1) ^ 1);
+                mbar_arrive(&sm->pfull[ps]);
+                continue;
+            }
+            float x[BN];
             tc_fence_after();
             const uint32_t s_addr = lane_base + kColS + s * BN;
             BA_TMEM_LD16(s_addr + 0, x, 0);
@@ -325,43 +437,37 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             tc_wait_ld();
             tc_fence_before();
             mbar_arrive(&sm->sempty[s]);
+            BA_STAMP(0);
 
             if (prm.dbg_S && head == prm.dbg_head && row_ok) {
 #pragma unroll
                 for (int i = 0; i < BN; ++i)
                     if (i < nk) prm.dbg_S[(int64_t)row * N + j * BN + i] = (int)x[i];
             }
-            // scores in the base-2 domain; masked columns -> -inf
-            if (bias_row) {
+            if (BIAS == 1) {
+                mbar_wait(&sm->bfull[bs], bn & 1);
+                const unsigned char* brow = sB + bs * 16384 + tid * 128;  // row tid of the 128 x 64 bf16 tile
 #pragma unroll
                 for (int c = 0; c < BN / 8; ++c) {
-                    const int col = j * BN + c * 8;
-                    if (bias_vec && col + 8 <= N) {
-                        const uint4 b = __ldg(reinterpret_cast<const uint4*>(bias_row + (int64_t)col * 2));
-                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+                    const uint4 b = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));  // 128B swizzle
+                    const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc2, __uint_as_float(bw[e] << 16) * kLog2e);
-                            x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc2, __uint_as_float(bw[e] & 0xFFFF0000u) * kLog2e);
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const float bv = (col + e < N) ? load_as_float(bias_row, a.bias_dtype, col + e) : 0.f;
-                            x[c * 8 + e] = fmaf(x[c * 8 + e], sc2, bv * kLog2e);
-                        }
+                    for (int e = 0; e < 4; ++e) {
+                        x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc, __uint_as_float(bw[e] << 16));
+                        x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc, __uint_as_float(bw[e] & 0xFFFF0000u));
                     }
                 }
-            } else {
+                mbar_arrive(&sm->bempty[bs]);
+            } else if (BIAS == 2) {
 #pragma unroll
-                for (int i = 0; i < BN; ++i) x[i] *= sc2;
+                for (int i = 0; i < BN; ++i) {
+                    const float bv = (bias_row && i < nk) ? load_as_float(bias_row, a.bias_dtype, j * BN + i) : 0.f;
+                    x[i] = fmaf(x[i], sc, bv);
+                }
             }
-            float tmax = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < BN; ++i) {
-                x[i] = (i < nk) ? x[i] : -INFINITY;
-                tmax = fmaxf(tmax, x[i]);
-            }
+            BA_STAMP(0);
+            float tmax = (nk == BN) ? tile_max<false>(x, nk) : tile_max<true>(x, nk);
+            tmax *= ea;  // ea >= 0, so the max commutes with the scaling
             m_true = fmaxf(m_true, tmax);
             // lazy rescale (first tile: m_ref = -inf forces it with alpha = 0 on the still-unwritten O)
             const bool need = tmax > m_ref + kRescaleThreshold;
@@ -369,9 +475,10 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 const float m_new = need ? tmax : m_ref;
                 const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
                 if (j > 0) {
-                    mbar_wait(&sm->pempty[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P.V of tile j-1 has landed in O
+                    const int qs = p2 ? ((j - 1) & 1) : 0, qn = p2 ? ((j - 1) >> 1) : (j - 1);
+                    mbar_wait(&sm->pempty[qs], qn & 1);  // P.V of tile j-1 has landed in O
                     tc_fence_after();
-                    for (int c = 0; c < prm.dvp; c += 16) {
+                    for (int c = 0; c < ocols; c += 16) {
                         float o[16];
                         BA_TMEM_LD16(lane_base + kColO + c, o, 0);
                         tc_wait_ld();
@@ -385,50 +492,60 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 l *= alpha;
                 m_ref = m_new;
             }
-            mbar_wait(&sm->pempty[s], (n & 1) ^ 1);  // P.V of tile j-2 no longer reads this P stage
-            unsigned char* prow = sP + s * 16384 + tid * 16;
+            BA_STAMP(0);
+            uint32_t pk[BN / 2];
+            if (nk == BN) l += exp_pack<false, !ROWSUM>(x, nk, ea, -m_ref, pk);
+            else l += exp_pack<true, !ROWSUM>(x, nk, ea, -m_ref, pk);
+            BA_STAMP(0);
+            mbar_wait(&sm->pempty[ps], (pn & 1) ^ 1);  // the previous P.V on this stage no longer reads it
+            BA_STAMP(0);
+            unsigned char* prow = sP + ps * 16384 + tid * 16;
 #pragma unroll
-            for (int c = 0; c < BN / 8; ++c) {
-                float p[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    p[e] = ex2(x[c * 8 + e] - m_ref);
-                    l += p[e];
-                }
-                uint4 v;
-                v.x = pack_bf16(p[0], p[1]);
-                v.y = pack_bf16(p[2], p[3]);
-                v.z = pack_bf16(p[4], p[5]);
-                v.w = pack_bf16(p[6], p[7]);
-                *reinterpret_cast<uint4*>(prow + c * (BM * 16)) = v;  // column chunk c, row tid: K-major core matrices
-            }
+            for (int c = 0; c < BN / 8; ++c)  // column chunk c, row tid: K-major core matrices
+                *reinterpret_cast<uint4*>(prow + c * (BM * 16)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
             fence_proxy_async();
-            mbar_arrive(&sm->pfull[s]);
+            mbar_arrive(&sm->pfull[ps]);
+            BA_STAMP(0);
         }
         // ---------------------------------------------------------------- epilogue: O / l
-        mbar_wait(&sm->pempty[(T - 1) & 1], ((T - 1) >> 1) & 1);
-        tc_fence_after();
-        const float inv_l = 1.0f / l;
-        float* orow = a.O + ((int64_t)head * N + row) * d;
-        for (int c = 0; c < prm.dvp; c += 16) {
-            float o[16];
-            BA_TMEM_LD16(lane_base + kColO + c, o, 0);
-            tc_wait_ld();
-            if (row_ok) {
-#pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                    if (c + i < d)
-                        *reinterpret_cast<float4*>(orow + c + i) =
-                            make_float4(o[i] * inv_l, o[i + 1] * inv_l, o[i + 2] * inv_l, o[i + 3] * inv_l);
+        {
+            const int t = T - 1;
+            const int ps = p2 ? (t & 1) : 0, pn = p2 ? (t >> 1) : t;
+            mbar_wait(&sm->pempty[ps], pn & 1);
+        }
+        BA_STAMP(0);
+        if (warp_ok) {
+            tc_fence_after();
+            if (ROWSUM) {  // denominator = first column of the ones block (sum of the bf16 weights the MMA used)
+                float o[16];
+                BA_TMEM_LD16(lane_base + kColO + prm.dvp, o, 0);
+                tc_wait_ld();
+                l = o[0];
             }
+            const float inv_l = 1.0f / l;
+            float* orow = a.O + ((int64_t)head * N + row) * d;
+            for (int c = 0; c < prm.dvp; c += 16) {
+                float o[16];
+                BA_TMEM_LD16(lane_base + kColO + c, o, 0);
+                tc_wait_ld();
+                if (row_ok) {
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        if (c + i < d)
+                            *reinterpret_cast<float4*>(orow + c + i) =
+                                make_float4(o[i] * inv_l, o[i + 1] * inv_l, o[i + 2] * inv_l, o[i + 3] * inv_l);
+                }
+            }
+            if (row_ok) {
+                if (a.row_max) a.row_max[(int64_t)head * N + row] = m_true * kLn2;
+                if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l * ex2(m_ref - m_true);
+            }
+            tc_fence_before();
         }
-        if (row_ok) {
-            if (a.row_max) a.row_max[(int64_t)head * N + row] = m_true * kLn2;
-            if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l * ex2(m_ref - m_true);
-        }
-        tc_fence_before();
+        BA_STAMP(0);
     }
     __syncthreads();
+    BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
     if (warp == 4) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -454,20 +571,45 @@ static EncodeTiledFn get_encode() {
 
 static int32_t* g_dbg_S = nullptr;
 static int g_dbg_head = -1;
+static long long* g_dbg_T = nullptr;
+constexpr size_t kSmemBudget = 113 * 1024;  // two CTAs per SM (227 KB usable, 1 KB reserved per CTA)
 
-template <int KPAD>
-static int launch_kpad(const Params& prm, const CUtensorMap& vmap, cudaStream_t stream) {
-    const size_t smem = 2 * (size_t)prm.nbox * 8192 + 2 * 16384 + (size_t)BM * KPAD + 2 * (size_t)BN * KPAD + sizeof(Smem);
+static size_t smem_bytes(const Params& prm, int kpad) {
+    return 2 * (size_t)prm.nbox * 8192 + (size_t)prm.bstages * 16384 + (size_t)prm.pstages * 16384 + (size_t)BM * kpad +
+           2 * (size_t)BN * kpad + 512 + sizeof(Smem);
+}
+
+template <int KPAD, int BIAS>
+static int launch_variant(const Params& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(attn_tc_kernel<KPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)kSmemBudget);
         if (e != cudaSuccess) return -(int)e;
         configured = true;
     }
-    attn_tc_kernel<KPAD><<<(unsigned)(prm.a.BH * prm.mblocks), kThreads, smem, stream>>>(prm, vmap);
+    attn_tc_kernel<KPAD, BIAS><<<(unsigned)(prm.a.BH * prm.mblocks), kThreads, smem_bytes(prm, KPAD), stream>>>(prm, vmap, bmap);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
+}
+
+// Timeline build of two representative variants (dev tool; selected when a timeline buffer is registered).
+template <int KPAD, int BIAS>
+static int launch_timeline(const Params& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+    cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    attn_tc_kernel<KPAD, BIAS, true><<<(unsigned)(prm.a.BH * prm.mblocks), kThreads, smem_bytes(prm, KPAD), stream>>>(prm, vmap, bmap);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+template <int KPAD>
+static int launch_kpad(const Params& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap,
+                       cudaStream_t stream) {
+    switch (bias_mode) {
+        case 0: return launch_variant<KPAD, 0>(prm, vmap, bmap, stream);
+        case 1: return launch_variant<KPAD, 1>(prm, vmap, bmap, stream);
+        default: return launch_variant<KPAD, 2>(prm, vmap, bmap, stream);
+    }
 }
 
 }  // namespace tc
@@ -495,23 +637,54 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.nbox = (a.d + 63) / 64;
     prm.dbg_S = g_dbg_S;
     prm.dbg_head = g_dbg_head;
-
-    CUtensorMap vmap;
-    const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
-    const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 2, (cuuint64_t)a.N * a.d * 2};
-    const cuuint32_t box[3] = {64, (cuuint32_t)BN, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return -(int)cudaErrorInvalidValue;
-
+    prm.dbg_T = g_dbg_T;
     const int kpad = (a.d + 31) / 32 * 32;
+
+    // bias path: a bf16 table with 16-byte aligned rows is staged tile by tile with TMA; anything else is read directly
+    int bias_mode = 0;
+    if (a.bias) {
+        const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 &&
+                            reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
+        bias_mode = tma_ok ? 1 : 2;
+    }
+    // stage counts: as deep as fits two CTAs per SM
+    prm.pstages = 2;
+    prm.bstages = bias_mode == 1 ? 2 : 0;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.pstages = 1;
+    if (smem_bytes(prm, kpad) > kSmemBudget && prm.bstages == 2) prm.bstages = 1;
+
+    CUtensorMap vmap, bmap;
+    {
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 2, (cuuint64_t)a.N * a.d * 2};
+        const cuuint32_t box[3] = {64, (cuuint32_t)BN, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult r = enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return -(int)cudaErrorInvalidValue;
+    }
+    bmap = vmap;
+    if (bias_mode == 1) {
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.N, (cuuint64_t)a.N, (cuuint64_t)a.bias_heads};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.bias_ld * 2, (cuuint64_t)a.N * a.bias_ld * 2};
+        const cuuint32_t box[3] = {(cuuint32_t)BN, (cuuint32_t)BM, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult r = enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.bias), gdim, gstr, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return -(int)cudaErrorInvalidValue;
+    }
+    if (g_dbg_T) {
+        if (kpad == 64 && bias_mode == 1) return launch_timeline<64, 1>(prm, vmap, bmap, stream);
+        if (kpad == 64 && bias_mode == 0) return launch_timeline<64, 0>(prm, vmap, bmap, stream);
+        if (kpad == 128 && bias_mode == 0) return launch_timeline<128, 0>(prm, vmap, bmap, stream);
+    }
     switch (kpad) {
-        case 32: return launch_kpad<32>(prm, vmap, stream);
-        case 64: return launch_kpad<64>(prm, vmap, stream);
-        case 96: return launch_kpad<96>(prm, vmap, stream);
-        case 128: return launch_kpad<128>(prm, vmap, stream);
+        case 32: return launch_kpad<32>(prm, bias_mode, vmap, bmap, stream);
+        case 64: return launch_kpad<64>(prm, bias_mode, vmap, bmap, stream);
+        case 96: return launch_kpad<96>(prm, bias_mode, vmap, bmap, stream);
+        case 128: return launch_kpad<128>(prm, bias_mode, vmap, bmap, stream);
     }
     return -(int)cudaErrorInvalidValue;
 }
@@ -523,3 +696,5 @@ extern "C" void ba_debug_tcgen05_logits(int32_t* dev_S, int head) {
     ba::tc::g_dbg_S = dev_S;
     ba::tc::g_dbg_head = head;
 }
+// Dev hook: per-CTA clock64 timeline, [ctas][4 roles][128] int64 (zero-filled by the caller).
+extern "C" void ba_debug_tcgen05_timeline(long long* dev_T) { ba::tc::g_dbg_T = dev_T; }
