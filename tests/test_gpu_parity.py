@@ -123,8 +123,9 @@ def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None):
             assert err <= TOL_O, f"{kern}: head {h} max-abs {err:.3e}"
             # log-sum-exp is tile-invariant: m + ln(l)  (AttentionOutput::row_max/row_sum, attention.hpp:45-46)
             # (the tcgen05 kernel's row_sum is the sum of the bf16-rounded weights it actually multiplied with V,
-            #  accumulated by the tensor core: ~3e-4 relative from the fp64 sum; a diagnostic, not part of O)
-            np.testing.assert_allclose(m[0, h] + np.log(l[0, h]), om + np.log(ol), rtol=0, atol=1e-3)
+            #  accumulated by the tensor core: each weight is within 2^-9 relative of exp(S-m), so ln(l) is within
+            #  2e-3 of the fp64 value; a diagnostic, not part of O)
+            np.testing.assert_allclose(m[0, h] + np.log(l[0, h]), om + np.log(ol), rtol=0, atol=2.5e-3)
         results[kern] = O
     return results
 
