@@ -1,0 +1,187 @@
+// binattn_b200.hpp -- C++ host-side mirror of the reference operator API over the C ABI (binattn_cuda.h).
+//
+// Mirrors, name for name, the part of the reference a caller of the hot path touches:
+//   binattn::AttentionConfig / ::make        proj/include/binattn/attention.hpp:29-41, proj/src/attention.cpp:45-53
+//   binattn::AttentionOutput                 attention.hpp:43-48
+//   binattn::binary_attention_fused          attention.hpp:69-71 (attention.cpp:250-382)
+//   binattn::ShapeError / ValidationError    proj/include/binattn/errors.hpp:16-25   (thrown for the same conditions:
+//                                            attention.cpp:21-28 shapes / temperature / block sizes, :60-61 bias table)
+// and BASELINE.json's operator shape  binary_attention(Q, K, V, bias, scale) -> O.
+//
+// Header-only and templated on the matrix type so it can be compiled against the reference's own
+// binattn::DenseMatrix (tensor.hpp:25-53) without copying it: any type with rows(), cols(), data() (contiguous
+// row-major doubles exposing .data()/.size()) and a (rows, cols, std::vector<double>) constructor works.
+// The reference computes in fp64 on the host; this shim uploads the operands in the requested device precision:
+//   Precision::f32  -- values rounded to fp32; sign bits identical to the reference unless |x| < 1.4e-45
+//                      (CUDA-core kernel; use this when bit-identical packed signs matter for arbitrary doubles)
+//   Precision::bf16 -- values rounded to bf16 (tcgen05 kernel; what the benchmarks use; inputs that already are
+//                      bf16-representable -- e.g. activations of a bf16 model -- lose nothing)
+// Output O is fp32 on the device, widened to double here.  quantize_pv = true (the reference's int8 P.V mode) and
+// with_probs are not carried over (O-parity is defined against quantize_pv = false).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "binattn_cuda.h"
+
+namespace binattn::b200 {
+
+class Error : public std::runtime_error {  // errors.hpp:10-13
+public:
+    explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+class ShapeError : public Error {  // errors.hpp:16-19
+public:
+    explicit ShapeError(const std::string& msg) : Error(msg) {}
+};
+class ValidationError : public Error {  // errors.hpp:22-25
+public:
+    explicit ValidationError(const std::string& msg) : Error(msg) {}
+};
+class CudaError : public Error {
+public:
+    explicit CudaError(const std::string& msg) : Error(msg) {}
+};
+class UnsupportedError : public Error {
+public:
+    explicit UnsupportedError(const std::string& msg) : Error(msg) {}
+};
+
+inline void check(int rc) {
+    if (rc == BA_OK) return;
+    const std::string msg = ba_last_error();
+    switch (rc) {
+        case BA_ERR_SHAPE: throw ShapeError(msg);
+        case BA_ERR_VALIDATION: throw ValidationError(msg);
+        case BA_ERR_UNSUPPORTED: throw UnsupportedError(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+enum class Precision { f32, bf16 };
+
+// binattn::AttentionConfig (attention.hpp:29-41) with the dense form of BiasSpec (materialize_bias output).
+template <class DenseMatrixT>
+struct AttentionConfigT {
+    std::size_t seq_len = 0;
+    std::size_t head_dim = 0;
+    double temperature = 1.0;
+    std::size_t block_rows = 64;  // validated like the reference; the CUDA kernels choose their own tiles
+    std::size_t block_cols = 64;
+    bool quantize_pv = false;
+    std::optional<DenseMatrixT> bias;  // dense N x N table
+    Precision precision = Precision::f32;
+
+    static AttentionConfigT make(std::size_t n, std::size_t d) {  // attention.cpp:45-53
+        AttentionConfigT cfg;
+        cfg.seq_len = n;
+        cfg.head_dim = d;
+        cfg.temperature = std::sqrt(static_cast<double>(d));
+        cfg.block_rows = n < 64 ? n : 64;
+        cfg.block_cols = n < 64 ? n : 64;
+        return cfg;
+    }
+};
+
+template <class DenseMatrixT>
+struct AttentionOutputT {  // attention.hpp:43-48 (probs is never produced)
+    DenseMatrixT output;
+    std::vector<double> row_max;
+    std::vector<double> row_sum;
+};
+
+inline std::uint16_t to_bf16_bits(double x) {  // round-to-nearest-even
+    float f = static_cast<float>(x);
+    std::uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<std::uint16_t>(u >> 16);
+}
+
+// One ba_handle per device; not copyable.
+class Engine {
+public:
+    explicit Engine(int device = 0) { check(ba_create(device, &h_)); }
+    ~Engine() { ba_destroy(h_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+    ba_handle* handle() const { return h_; }
+
+    // binattn::binary_attention_fused(q, k, v, cfg): one head, N x d matrices.
+    template <class DenseMatrixT>
+    AttentionOutputT<DenseMatrixT> binary_attention_fused(const DenseMatrixT& q, const DenseMatrixT& k,
+                                                          const DenseMatrixT& v,
+                                                          const AttentionConfigT<DenseMatrixT>& cfg) const {
+        const std::size_t n = cfg.seq_len, d = cfg.head_dim;
+        // check_shapes, attention.cpp:17-29 (same messages, same exception types)
+        if (q.rows() != n || q.cols() != d) throw ShapeError("attention: Q must be N x d");
+        if (k.rows() != n || k.cols() != d) throw ShapeError("attention: K must be N x d");
+        if (v.rows() != n || v.cols() != d) throw ShapeError("attention: V must be N x d");
+        if (!(cfg.temperature > 0.0)) throw ValidationError("attention: temperature must be positive");
+        if (cfg.block_rows < 1 || cfg.block_rows > n || cfg.block_cols < 1 || cfg.block_cols > n)
+            throw ValidationError("attention: block sizes must be in [1, N]");
+        if (cfg.bias && (cfg.bias->rows() != n || cfg.bias->cols() != n))
+            throw ShapeError("bias: dense table must be N x N");  // attention.cpp:60-61
+        if (cfg.quantize_pv)
+            throw UnsupportedError("quantize_pv=true (int8 P.V) is not built: the CUDA path implements quantize_pv=false");
+        if (n == 0 || d == 0) throw ShapeError("binary_quantize: empty matrix");  // quantize.cpp:17
+
+        ba_params p{};
+        p.B = 1;
+        p.H = 1;
+        p.N = static_cast<int32_t>(n);
+        p.d = static_cast<int32_t>(d);
+        p.in_dtype = cfg.precision == Precision::bf16 ? BA_BF16 : BA_F32;
+        p.bias_mode = cfg.bias ? BA_BIAS_DENSE : BA_BIAS_NONE;
+        p.bias_heads = 1;
+        p.bias_dtype = BA_F32;
+        p.bias_ld = 0;
+        p.inv_tau = static_cast<float>(1.0 / cfg.temperature);
+        p.kernel = BA_KERNEL_AUTO;
+
+        std::vector<float> o(n * d), m(n), l(n), bias32;
+        if (cfg.bias) bias32.assign(cfg.bias->data().data(), cfg.bias->data().data() + n * n);
+        if (cfg.precision == Precision::bf16) {
+            std::vector<std::uint16_t> hq(n * d), hk(n * d), hv(n * d);
+            for (std::size_t i = 0; i < n * d; ++i) {
+                hq[i] = to_bf16_bits(q.data().data()[i]);
+                hk[i] = to_bf16_bits(k.data().data()[i]);
+                hv[i] = to_bf16_bits(v.data().data()[i]);
+            }
+            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), cfg.bias ? bias32.data() : nullptr,
+                                           o.data(), m.data(), l.data()));
+        } else {
+            std::vector<float> hq(q.data().data(), q.data().data() + n * d), hk(k.data().data(), k.data().data() + n * d),
+                hv(v.data().data(), v.data().data() + n * d);
+            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), cfg.bias ? bias32.data() : nullptr,
+                                           o.data(), m.data(), l.data()));
+        }
+        return AttentionOutputT<DenseMatrixT>{DenseMatrixT(n, d, std::vector<double>(o.begin(), o.end())),
+                                              std::vector<double>(m.begin(), m.end()),
+                                              std::vector<double>(l.begin(), l.end())};
+    }
+
+    // BASELINE.json operator: binary_attention(Q, K, V, bias, scale) -> O, scale = 1 / temperature.
+    template <class DenseMatrixT>
+    DenseMatrixT binary_attention(const DenseMatrixT& q, const DenseMatrixT& k, const DenseMatrixT& v,
+                                  const std::optional<DenseMatrixT>& bias, double scale,
+                                  Precision precision = Precision::f32) const {
+        if (!(scale > 0.0)) throw ValidationError("attention: temperature must be positive");
+        AttentionConfigT<DenseMatrixT> cfg = AttentionConfigT<DenseMatrixT>::make(q.rows(), q.cols());
+        cfg.temperature = 1.0 / scale;
+        cfg.bias = bias;
+        cfg.precision = precision;
+        return binary_attention_fused(q, k, v, cfg).output;
+    }
+
+private:
+    ba_handle* h_ = nullptr;
+};
+
+}  // namespace binattn::b200

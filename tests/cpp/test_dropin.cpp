@@ -1,0 +1,139 @@
+// test_dropin.cpp -- the reference's own attention test cases (proj/tests/test_attention.cpp) pointed at the
+// B200 path through include/binattn_b200.hpp, with the CPU oracle (oracle/binattn_oracle.c) as the checker.
+// Built and run by tests/test_cpp_dropin.py (-m gpu).  The matrix type below is a stand-in with the same
+// surface as binattn::DenseMatrix (tensor.hpp:25-53); the shim is templated so the real one works unchanged.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "binattn_b200.hpp"
+
+extern "C" {
+typedef struct bo_rng bo_rng;
+size_t bo_rng_sizeof(void);
+void bo_rng_init(void* r, uint64_t seed, uint64_t stream);
+void bo_random_dense(void* r, size_t count, double scale, double* out);
+int bo_binary_attention_fused(const double* q, const double* k, const double* v, size_t n, size_t d, double tau,
+                              size_t br, size_t bc, int qpv, const double* bias, double* y, double* m, double* l);
+}
+
+struct Span {
+    const double* p;
+    std::size_t n;
+    const double* data() const { return p; }
+    std::size_t size() const { return n; }
+};
+class Mat {  // same surface as binattn::DenseMatrix
+public:
+    Mat(std::size_t r, std::size_t c, std::vector<double> d) : r_(r), c_(c), d_(std::move(d)) {}
+    std::size_t rows() const { return r_; }
+    std::size_t cols() const { return c_; }
+    Span data() const { return {d_.data(), d_.size()}; }
+    double operator()(std::size_t i, std::size_t j) const { return d_[i * c_ + j]; }
+
+private:
+    std::size_t r_, c_;
+    std::vector<double> d_;
+};
+
+using namespace binattn::b200;
+using Cfg = AttentionConfigT<Mat>;
+static int failures = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);    \
+            ++failures;                                                    \
+        }                                                                  \
+    } while (0)
+
+static Mat random_dense(void* rng, std::size_t r, std::size_t c, double scale = 1.0) {  // oracles.hpp:19-25
+    std::vector<double> d(r * c);
+    bo_random_dense(rng, r * c, scale, d.data());
+    return Mat(r, c, std::move(d));
+}
+static double bf16_round(double x) {
+    uint32_t u = (uint32_t)to_bf16_bits(x) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+static Mat rounded(const Mat& m, Precision p) {
+    std::vector<double> d(m.data().data(), m.data().data() + m.rows() * m.cols());
+    for (double& x : d) x = p == Precision::bf16 ? bf16_round(x) : (double)(float)x;
+    return Mat(m.rows(), m.cols(), std::move(d));
+}
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    Engine eng(0);
+    std::vector<unsigned char> rng(bo_rng_sizeof());
+
+    {  // frozen fixture: d=1 N=2 binary attention by hand (test_attention.cpp:163-174)
+        const Mat q(2, 1, {2.0, -1.0}), k(2, 1, {1.0, -3.0}), v(2, 1, {4.0, -2.0});
+        Cfg cfg = Cfg::make(2, 1);
+        const auto out = eng.binary_attention_fused(q, k, v, cfg);
+        CHECK(std::fabs(out.row_max[0] - 3.0) < 1e-5);
+        CHECK(std::fabs(out.output(0, 0) - 3.985164261060192) < 1e-5);
+        CHECK(std::fabs(out.output(1, 0) - -1.9851642610601914) < 1e-5);
+    }
+    {  // shape mismatches raise ShapeError, bad block sizes ValidationError (test_attention.cpp:126-141)
+        bo_rng_init(rng.data(), 33, 0);
+        const Mat q = random_dense(rng.data(), 4, 3), bad = random_dense(rng.data(), 4, 2), v = random_dense(rng.data(), 4, 3);
+        Cfg cfg = Cfg::make(4, 3);
+        CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(q, bad, v, cfg); }));
+        CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(bad, q, v, cfg); }));
+        CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(q, v, bad, cfg); }));
+        Cfg big = cfg;
+        big.block_rows = 9;
+        CHECK(throws<ValidationError>([&] { eng.binary_attention_fused(q, q, v, big); }));
+        Cfg cold = cfg;
+        cold.temperature = 0.0;
+        CHECK(throws<ValidationError>([&] { eng.binary_attention_fused(q, q, v, cold); }));
+        Cfg b = cfg;
+        b.bias = Mat(3, 3, std::vector<double>(9, 0.0));
+        CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(q, q, v, b); }));  // attention.cpp:60-61
+    }
+    // seeded cases of the reference suite + the BASELINE head shapes, both precisions, with and without dense bias
+    struct Case { uint64_t seed; std::size_t n, d; double bias_scale; };
+    const Case cases[] = {{35, 12, 16, 0.0}, {38, 48, 16, 0.4}, {40, 64, 32, 0.0}, {43, 50, 12, 0.0},
+                          {0, 197, 64, 0.5}, {1, 256, 72, 0.5}, {2, 130, 128, 0.5}};
+    for (const Case& c : cases) {
+        for (Precision prec : {Precision::f32, Precision::bf16}) {
+            bo_rng_init(rng.data(), c.seed, 0);
+            const Mat q = rounded(random_dense(rng.data(), c.n, c.d), prec), k = rounded(random_dense(rng.data(), c.n, c.d), prec),
+                      v = rounded(random_dense(rng.data(), c.n, c.d), prec);
+            Cfg cfg = Cfg::make(c.n, c.d);
+            cfg.precision = prec;
+            if (c.bias_scale > 0) cfg.bias = rounded(random_dense(rng.data(), c.n, c.n, c.bias_scale), Precision::f32);
+            const auto out = eng.binary_attention_fused(q, k, v, cfg);
+            std::vector<double> y(c.n * c.d), m(c.n), l(c.n);
+            const int rc = bo_binary_attention_fused(q.data().data(), k.data().data(), v.data().data(), c.n, c.d,
+                                                     cfg.temperature, cfg.block_rows, cfg.block_cols, 0,
+                                                     cfg.bias ? cfg.bias->data().data() : nullptr, y.data(), m.data(), l.data());
+            CHECK(rc == 0);
+            double worst = 0.0;
+            for (std::size_t i = 0; i < c.n * c.d; ++i) worst = std::fmax(worst, std::fabs(out.output.data().data()[i] - y[i]));
+            std::printf("seed %llu N=%zu d=%zu %s bias=%d  max_abs=%.3e\n", (unsigned long long)c.seed, c.n, c.d,
+                        prec == Precision::bf16 ? "bf16" : "f32", c.bias_scale > 0, worst);
+            CHECK(worst <= 2e-3);
+            // operator form: binary_attention(Q, K, V, bias, scale)
+            const Mat o2 = eng.binary_attention(q, k, v, cfg.bias, 1.0 / cfg.temperature, prec);
+            for (std::size_t i = 0; i < c.n * c.d; ++i) CHECK(o2.data().data()[i] == out.output.data().data()[i]);
+        }
+    }
+    std::printf(failures ? "FAILED (%d)\n" : "ALL OK\n", failures);
+    return failures ? 1 : 0;
+}
