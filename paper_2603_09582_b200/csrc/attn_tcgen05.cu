@@ -24,6 +24,8 @@
 // TMEM read-modify-write traffic off the common path; the final O/l is unaffected (both carry the same reference max).
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "ba_common.cuh"
 
 namespace ba {
@@ -46,6 +48,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// One arrival on behalf of the whole warp: every lane's preceding work is ordered before it by the warp barrier
+// (128 per-thread arrivals on one mbarrier serialise in the shared-memory atomic unit and slow every barrier op).
+__device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -335,14 +343,14 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     // ---------------------------------------------------------------- prologue
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm->kfull[s], 64);    // every expander thread arrives
+            mbar_init(&sm->kfull[s], 2);     // one elected arrival per expander warp
             mbar_init(&sm->vfull[s], 1);     // expect_tx arrive + TMA bytes
             mbar_init(&sm->sdone[s], 1);     // tcgen05.commit after the S MMA of a tile
-            mbar_init(&sm->sempty[s], 128);  // every softmax thread arrives (S stage read out)
-            mbar_init(&sm->pfull[s], 128);   // every softmax thread arrives (P stage written)
+            mbar_init(&sm->sempty[s], 4);    // one elected arrival per softmax warp (S stage read out)
+            mbar_init(&sm->pfull[s], 4);     // one elected arrival per softmax warp (P stage written)
             mbar_init(&sm->pvdone[s], 1);    // tcgen05.commit after the P.V MMA of a tile
             mbar_init(&sm->bfull[s], 1);     // expect_tx arrive + TMA bytes
-            mbar_init(&sm->bempty[s], 128);  // every softmax thread arrives (bias stage read out)
+            mbar_init(&sm->bempty[s], 4);    // one elected arrival per softmax warp (bias stage read out)
         }
         fence_barrier_init();
     }
@@ -410,7 +418,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         };
         for (int j = 0; j < T; ++j) {
             const int s = j & 1, n = j >> 1;
-            const uint32_t s_ok = mbar_try(&sm->sempty[s], (n & 1) ^ 1);
+            const uint32_t s_ok = n > 0 ? mbar_try(&sm->sempty[s], (n & 1) ^ 1) : 1u;  // first use: stage is free
             mbar_wait(&sm->kfull[s], n & 1);
             if (!s_ok) mbar_wait(&sm->sempty[s], (n & 1) ^ 1);
             BA_STAMP(1);
@@ -433,12 +441,12 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 const int s = j & 1, n = j >> 1;
                 if (BIAS == 1) {
                     const int bs = b2 ? s : 0, bn = b2 ? n : j;
-                    mbar_wait(&sm->bempty[bs], (bn & 1) ^ 1);
+                    if (bn > 0) mbar_wait(&sm->bempty[bs], (bn & 1) ^ 1);
                     mbar_expect_tx(&sm->bfull[bs], 16384);
                     tma_load_3d(&bmap, &sm->bfull[bs], sB + bs * 16384, j * BN, row0, bh);
                 }
                 BA_STAMP(2);
-                mbar_wait(&sm->pvdone[s], (n & 1) ^ 1);  // P.V of tile j-2 released this V stage
+                if (n > 0) mbar_wait(&sm->pvdone[s], (n & 1) ^ 1);  // P.V of tile j-2 released this V stage
                 BA_STAMP(2);
                 mbar_expect_tx(&sm->vfull[s], prm.nbox * 8192);
                 for (int b = 0; b < prm.nbox; ++b)
@@ -451,12 +459,12 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         for (int j = 0; j < T; ++j) {
             const int s = j & 1, n = j >> 1;
             const int key = j * BN + t;
-            mbar_wait(&sm->sdone[s], (n & 1) ^ 1);  // S MMA of tile j-2 released this K stage
+            if (n > 0) mbar_wait(&sm->sdone[s], (n & 1) ^ 1);  // S MMA of tile j-2 released this K stage
             BA_STAMP(3);
             expand_store<KPAD>(sK + s * BN * KPAD, BN, t, w32, d, key < N, sm->lut);
             BA_STAMP(3);
             fence_proxy_async();
-            mbar_arrive(&sm->kfull[s]);
+            warp_arrive(&sm->kfull[s], lane);
             BA_STAMP(3);
             // prefetch the next tile's words so their L2 latency hides behind the next wait
             if (j + 1 < T) load_words<KPAD>(w32, a.k_words + ((int64_t)head * N + key + BN) * w64, w64, key + BN < N);
@@ -488,13 +496,13 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             if (!s_ok) mbar_wait(&sm->sdone[s], n & 1);
             BA_STAMP(0);
             if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
-                mbar_arrive(&sm->sempty[s]);
+                warp_arrive(&sm->sempty[s], lane);
                 if (BIAS == 1) {
                     mbar_wait(&sm->bfull[bs], bn & 1);
-                    mbar_arrive(&sm->bempty[bs]);
+                    warp_arrive(&sm->bempty[bs], lane);
                 }
                 if (jf >= 0) mbar_wait(&sm->pvdone[jf & 1], (jf >> 1) & 1);
-                mbar_arrive(&sm->pfull[ps]);
+                warp_arrive(&sm->pfull[ps], lane);
                 s_ok = (j + 1 < T) ? mbar_try(&sm->sdone[s ^ 1], ((j + 1) >> 1) & 1) : 1u;
                 continue;
             }
@@ -510,7 +518,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             const uint32_t p_ok = jf >= 0 ? mbar_try(&sm->pvdone[jf & 1], (jf >> 1) & 1) : 1u;
             tc_wait_ld();
             tc_fence_before();
-            mbar_arrive(&sm->sempty[s]);
+            warp_arrive(&sm->sempty[s], lane);
             BA_STAMP(0);
 
             if (prm.dbg_S && head == prm.dbg_head && row_ok) {
@@ -524,7 +532,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
 #pragma unroll
                 for (int c = 0; c < BN / 16; ++c)
                     if (c < nch) bias_chunk<1>(x, c, sc, brow, tid, nullptr, 0, 0, nk);
-                mbar_arrive(&sm->bempty[bs]);
+                warp_arrive(&sm->bempty[bs], lane);
             } else if (BIAS == 2) {
 #pragma unroll
                 for (int c = 0; c < BN / 16; ++c)
@@ -563,7 +571,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             else l += exp_store<true, !ROWSUM>(x, nk, nch, ea, -m_ref, prow);
             BA_STAMP(0);
             fence_proxy_async();
-            mbar_arrive(&sm->pfull[ps]);
+            warp_arrive(&sm->pfull[ps], lane);
             s_ok = (j + 1 < T) ? mbar_try(&sm->sdone[s ^ 1], ((j + 1) >> 1) & 1) : 1u;
             BA_STAMP(0);
         }
@@ -637,10 +645,16 @@ static EncodeTiledFn get_encode() {
 static int32_t* g_dbg_S = nullptr;
 static int g_dbg_head = -1;
 static long long* g_dbg_T = nullptr;
-constexpr size_t kSmemBudget = 113 * 1024;  // two CTAs per SM (227 KB usable, 1 KB reserved per CTA)
+constexpr size_t kSmemBudget = 113 * 1024;
+constexpr size_t kSmemMax = 227 * 1024;  // two CTAs per SM (227 KB usable, 1 KB reserved per CTA)
 
+static size_t smem_pad() {  // dev knob: BA_SMEM_PAD=<bytes> forces lower occupancy for experiments
+    static long pad = -1;
+    if (pad < 0) { const char* e = getenv("BA_SMEM_PAD"); pad = e ? atol(e) : 0; }
+    return (size_t)pad;
+}
 static size_t smem_bytes(const Params& prm, int kpad) {
-    return 2 * (size_t)prm.nbox * 8192 + (size_t)prm.bstages * 16384 + (size_t)prm.pstages * 16384 + (size_t)BM * kpad +
+    return smem_pad() + 2 * (size_t)prm.nbox * 8192 + (size_t)prm.bstages * 16384 + (size_t)prm.pstages * 16384 + (size_t)BM * kpad +
            2 * (size_t)BN * kpad + 512 + sizeof(Smem);
 }
 
@@ -653,7 +667,7 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
     static bool configured = false;
     if (!configured) {
         const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)kSmemBudget);
+                                                   (int)kSmemMax);
         if (e != cudaSuccess) return -(int)e;
         configured = true;
     }
