@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
     const char* bias_row = nullptr;
     if (a.bias && row_ok)
         bias_row = static_cast<const char*>(a.bias) +
-                   ((int64_t)(head % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                   ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
 
     float o[kSimtSlice];
 #pragma unroll

@@ -436,7 +436,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     } else if (warp == 5) {
         // ============================================================ TMA producer (V tiles, bias tiles)
         if (lane == 0) {
-            const int bh = head % a.H % a.bias_heads;
+            const int bh = (a.head0 + head) % a.H % a.bias_heads;
             for (int j = 0; j < T; ++j) {
                 const int s = j & 1, n = j >> 1;
                 if (BIAS == 1) {
@@ -480,7 +480,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         const char* bias_row = nullptr;
         if (BIAS == 2 && row_ok)
             bias_row = static_cast<const char*>(a.bias) +
-                       ((int64_t)(head % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                       ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
         float m_ref = -INFINITY, m_true = -INFINITY, l = 0.f;  // base-2 units
         uint32_t s_ok = mbar_try(&sm->sdone[0], 0);
 

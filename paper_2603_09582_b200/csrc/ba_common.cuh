@@ -27,6 +27,7 @@ struct FwdArgs {
     int64_t bias_ld;
     int BH, H, N, d, W64;
     int bias_heads;
+    int head0;                // index of this call's first head in the caller's [B*H] grid (bias table = (head0+head) % H % bias_heads)
     int bias_dtype;
     int in_dtype;
     float inv_tau;

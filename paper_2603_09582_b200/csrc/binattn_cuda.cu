@@ -42,9 +42,9 @@ struct Layout {
     int W64, chunks;
 };
 
-Layout make_layout(const ba_params* p) {
+Layout make_layout(const ba_params* p, int64_t heads = -1) {
     Layout L{};
-    L.BH = (int64_t)p->B * p->H;
+    L.BH = heads >= 0 ? heads : (int64_t)p->B * p->H;
     L.W64 = (p->d + 63) / 64;
     L.chunks = ba::pack_partials_per_head(p->N, p->d, p->in_dtype);
     const size_t plane = align_up((size_t)L.BH * p->N * L.W64 * sizeof(uint64_t), 256);
@@ -83,6 +83,8 @@ int check_params(const ba_params* p, bool need_attention) {
 
 }  // namespace
 
+constexpr int kHostChunksMax = 32;
+
 struct ba_handle {
     int device = 0;
     int64_t launches = 0;
@@ -92,10 +94,11 @@ struct ba_handle {
     size_t tickets_n = 0;
     float* partials = nullptr;  // for standalone ba_pack_signs
     size_t partials_n = 0;
-    // host-buffer path
-    cudaStream_t stream = nullptr;
-    void* stage[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t stage_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
+    // host-buffer path: copy-in stream, compute stream, copy-out stream + per-chunk events
+    cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
+    cudaEvent_t ev_in[kHostChunksMax] = {}, ev_done[kHostChunksMax] = {};
+    void* stage[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t stage_bytes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // per-kernel profiling (ba_profile_begin/end)
     cudaEvent_t* prof_ev = nullptr;
     int prof_cap = 0, prof_n = 0;
@@ -148,9 +151,15 @@ int ba_create(int device, ba_handle** out) {
     ba_handle* h = new ba_handle();
     h->device = device;
     e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream_out, cudaStreamNonBlocking);
+    for (int i = 0; i < kHostChunksMax && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
-        delete h;
-        return fail(BA_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+        ba_destroy(h);
+        return fail(BA_ERR_CUDA, "cudaStreamCreate/cudaEventCreate: %s", cudaGetErrorString(e));
     }
     *out = h;
     return BA_OK;
@@ -165,6 +174,12 @@ int ba_destroy(ba_handle* h) {
     for (void* s : h->stage)
         if (s) cudaFree(s);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->stream_in) cudaStreamDestroy(h->stream_in);
+    if (h->stream_out) cudaStreamDestroy(h->stream_out);
+    for (int i = 0; i < kHostChunksMax; ++i) {
+        if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+    }
     delete h;
     return BA_OK;
 }
@@ -266,32 +281,12 @@ int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, 
     return BA_OK;
 }
 
-int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
-                            const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
-                            void* stream_) {
-    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
-    int rc = check_params(p, true);
-    if (rc) return rc;
-    if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
-    if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
-    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-    BA_CUDA(cudaSetDevice(h->device));
-
-    const char* why = "";
-    const bool tc_ok = ba::tcgen05_supported(p, &why);
-    int kernel = p->kernel;
-    if (kernel == BA_KERNEL_AUTO) kernel = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
-    if (kernel == BA_KERNEL_TCGEN05 && !tc_ok) return fail(BA_ERR_UNSUPPORTED, "tcgen05 kernel: %s", why);
-    if (kernel != BA_KERNEL_TCGEN05 && kernel != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");
-
-    const Layout L = make_layout(p);
-    if (!workspace) {
-        if ((rc = ensure(&h->ws, &h->ws_bytes, L.total, false))) return rc;
-        workspace = h->ws;
-    }
-    if ((rc = ensure_tickets(h, 2 * (size_t)L.BH))) return rc;
-    char* ws = static_cast<char*>(workspace);
-
+// One K1 + K2 pass over `heads` consecutive heads starting at grid index head0; every tensor pointer already points at
+// that first head.  `ws` holds make_layout(p, heads).total bytes, `tickets` 2*heads zeroed counters.
+static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0, int64_t heads, const void* Q, const void* K,
+                     const void* V, const void* bias, float* O, float* row_max, float* row_sum, char* ws,
+                     unsigned int* tickets, cudaStream_t stream, bool prof) {
+    const Layout L = make_layout(p, heads);
     ba::FwdArgs a{};
     a.V = V;
     a.q_words = reinterpret_cast<uint64_t*>(ws + L.q_words);
@@ -303,23 +298,22 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     a.row_max = row_max;
     a.row_sum = row_sum;
     a.bias_ld = p->bias_ld ? p->bias_ld : p->N;
-    a.BH = (int)L.BH;
+    a.BH = (int)heads;
     a.H = p->H;
     a.N = p->N;
     a.d = p->d;
     a.W64 = L.W64;
     a.bias_heads = p->bias_mode == BA_BIAS_DENSE ? p->bias_heads : 1;
+    a.head0 = (int)(head0 % p->H);
     a.bias_dtype = p->bias_dtype;
     a.in_dtype = p->in_dtype;
     a.inv_tau = p->inv_tau;
 
-    const bool prof = h->prof_ev && h->prof_n < h->prof_cap;
     cudaEvent_t* ev = prof ? h->prof_ev + 3 * h->prof_n : nullptr;
     if (prof) BA_CUDA(cudaEventRecord(ev[0], stream));
-    int n = ba::launch_pack_signs_qk(Q, K, p->in_dtype, L.BH, p->N, p->d, const_cast<uint64_t*>(a.q_words),
+    int n = ba::launch_pack_signs_qk(Q, K, p->in_dtype, heads, p->N, p->d, const_cast<uint64_t*>(a.q_words),
                                      const_cast<uint64_t*>(a.k_words), const_cast<float*>(a.mu_q),
-                                     const_cast<float*>(a.mu_k), reinterpret_cast<float*>(ws + L.partials), h->tickets,
-                                     stream);
+                                     const_cast<float*>(a.mu_k), reinterpret_cast<float*>(ws + L.partials), tickets, stream);
     if (n < 0) return fail(BA_ERR_CUDA, "pack_signs launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
     if (prof) BA_CUDA(cudaEventRecord(ev[1], stream));
@@ -333,6 +327,42 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     return BA_OK;
 }
 
+static int resolve_kernel(const ba_params* p, int* kernel) {
+    const char* why = "";
+    const bool tc_ok = ba::tcgen05_supported(p, &why);
+    int k = p->kernel;
+    if (k == BA_KERNEL_AUTO) k = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
+    if (k == BA_KERNEL_TCGEN05 && !tc_ok) return fail(BA_ERR_UNSUPPORTED, "tcgen05 kernel: %s", why);
+    if (k != BA_KERNEL_TCGEN05 && k != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");
+    *kernel = k;
+    return BA_OK;
+}
+
+int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
+                            const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
+                            void* stream_) {
+    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
+    int rc = check_params(p, true);
+    if (rc) return rc;
+    if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
+    if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    BA_CUDA(cudaSetDevice(h->device));
+    int kernel = 0;
+    if ((rc = resolve_kernel(p, &kernel))) return rc;
+    const Layout L = make_layout(p);
+    if (!workspace) {
+        if ((rc = ensure(&h->ws, &h->ws_bytes, L.total, false))) return rc;
+        workspace = h->ws;
+    }
+    if ((rc = ensure_tickets(h, 2 * (size_t)L.BH))) return rc;
+    const bool prof = h->prof_ev && h->prof_n < h->prof_cap;
+    return fwd_range(h, p, kernel, 0, L.BH, Q, K, V, bias, O, row_max, row_sum, static_cast<char*>(workspace), h->tickets,
+                     stream, prof);
+}
+
+// Host-buffer call: the head grid is cut into chunks that flow through three streams -- H2D copies, K1+K2, D2H copies
+// -- so the two PCIe directions and the kernels overlap (the copies are asynchronous only for pinned host memory).
 int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
                              const void* bias, float* O, float* row_max, float* row_sum) {
     if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
@@ -341,30 +371,63 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
     if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
     BA_CUDA(cudaSetDevice(h->device));
+    int kernel = 0;
+    if ((rc = resolve_kernel(p, &kernel))) return rc;
     const size_t BH = (size_t)p->B * p->H;
-    const size_t in_bytes = BH * p->N * p->d * ba::dtype_size(p->in_dtype);
-    const size_t out_bytes = BH * p->N * p->d * sizeof(float);
+    const size_t head_in = (size_t)p->N * p->d * ba::dtype_size(p->in_dtype);  // bytes of one head of Q, K or V
+    const size_t head_out = (size_t)p->N * p->d * sizeof(float);
+    const size_t head_row = (size_t)p->N * sizeof(float);
     const size_t ld = p->bias_ld ? p->bias_ld : p->N;
     const size_t bias_bytes =
         p->bias_mode == BA_BIAS_DENSE ? (size_t)p->bias_heads * p->N * ld * ba::dtype_size(p->bias_dtype) : 0;
-    const size_t row_bytes = BH * p->N * sizeof(float);
-    const size_t need[7] = {in_bytes, in_bytes, in_bytes, bias_bytes, out_bytes, row_max ? row_bytes : 0,
-                            row_sum ? row_bytes : 0};
-    for (int i = 0; i < 7; ++i)
+    // chunking: about 4 MB of each input per chunk, at most kHostChunksMax chunks
+    size_t per = (4u << 20) / head_in;
+    if (per < 1) per = 1;
+    if ((BH + per - 1) / per > (size_t)kHostChunksMax) per = (BH + kHostChunksMax - 1) / kHostChunksMax;
+    const int chunks = (int)((BH + per - 1) / per);
+    const Layout Lc = make_layout(p, (int64_t)per);
+    const size_t need[8] = {BH * head_in, BH * head_in, BH * head_in, bias_bytes, BH * head_out,
+                            row_max ? BH * head_row : 0, row_sum ? BH * head_row : 0, (size_t)chunks * Lc.total};
+    for (int i = 0; i < 8; ++i)
         if (need[i] && (rc = ensure(&h->stage[i], &h->stage_bytes[i], need[i], false))) return rc;
-    cudaStream_t s = h->stream;
-    BA_CUDA(cudaMemcpyAsync(h->stage[0], Q, in_bytes, cudaMemcpyHostToDevice, s));
-    BA_CUDA(cudaMemcpyAsync(h->stage[1], K, in_bytes, cudaMemcpyHostToDevice, s));
-    BA_CUDA(cudaMemcpyAsync(h->stage[2], V, in_bytes, cudaMemcpyHostToDevice, s));
-    if (bias_bytes) BA_CUDA(cudaMemcpyAsync(h->stage[3], bias, bias_bytes, cudaMemcpyHostToDevice, s));
-    rc = ba_binary_attention_fwd(h, p, h->stage[0], h->stage[1], h->stage[2], bias_bytes ? h->stage[3] : nullptr,
-                                 static_cast<float*>(h->stage[4]), row_max ? static_cast<float*>(h->stage[5]) : nullptr,
-                                 row_sum ? static_cast<float*>(h->stage[6]) : nullptr, nullptr, s);
-    if (rc) return rc;
-    BA_CUDA(cudaMemcpyAsync(O, h->stage[4], out_bytes, cudaMemcpyDeviceToHost, s));
-    if (row_max) BA_CUDA(cudaMemcpyAsync(row_max, h->stage[5], row_bytes, cudaMemcpyDeviceToHost, s));
-    if (row_sum) BA_CUDA(cudaMemcpyAsync(row_sum, h->stage[6], row_bytes, cudaMemcpyDeviceToHost, s));
-    BA_CUDA(cudaStreamSynchronize(s));
+    if ((rc = ensure_tickets(h, 2 * BH))) return rc;
+    char* const dQ = static_cast<char*>(h->stage[0]);
+    char* const dK = static_cast<char*>(h->stage[1]);
+    char* const dV = static_cast<char*>(h->stage[2]);
+    char* const dO = static_cast<char*>(h->stage[4]);
+    char* const dM = static_cast<char*>(h->stage[5]);
+    char* const dL = static_cast<char*>(h->stage[6]);
+    if (bias_bytes) BA_CUDA(cudaMemcpyAsync(h->stage[3], bias, bias_bytes, cudaMemcpyHostToDevice, h->stream_in));
+    for (int c = 0; c < chunks; ++c) {
+        const size_t h0 = (size_t)c * per, nh = (h0 + per <= BH) ? per : BH - h0;
+        BA_CUDA(cudaMemcpyAsync(dQ + h0 * head_in, static_cast<const char*>(Q) + h0 * head_in, nh * head_in,
+                                cudaMemcpyHostToDevice, h->stream_in));
+        BA_CUDA(cudaMemcpyAsync(dK + h0 * head_in, static_cast<const char*>(K) + h0 * head_in, nh * head_in,
+                                cudaMemcpyHostToDevice, h->stream_in));
+        BA_CUDA(cudaMemcpyAsync(dV + h0 * head_in, static_cast<const char*>(V) + h0 * head_in, nh * head_in,
+                                cudaMemcpyHostToDevice, h->stream_in));
+        BA_CUDA(cudaEventRecord(h->ev_in[c], h->stream_in));
+        BA_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
+        rc = fwd_range(h, p, kernel, (int64_t)h0, (int64_t)nh, dQ + h0 * head_in, dK + h0 * head_in, dV + h0 * head_in,
+                       bias_bytes ? h->stage[3] : nullptr, reinterpret_cast<float*>(dO + h0 * head_out),
+                       row_max ? reinterpret_cast<float*>(dM + h0 * head_row) : nullptr,
+                       row_sum ? reinterpret_cast<float*>(dL + h0 * head_row) : nullptr,
+                       static_cast<char*>(h->stage[7]) + (size_t)c * Lc.total, h->tickets + 2 * h0, h->stream, false);
+        if (rc) return rc;
+        BA_CUDA(cudaEventRecord(h->ev_done[c], h->stream));
+        BA_CUDA(cudaStreamWaitEvent(h->stream_out, h->ev_done[c], 0));
+        BA_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(O) + h0 * head_out, dO + h0 * head_out, nh * head_out,
+                                cudaMemcpyDeviceToHost, h->stream_out));
+        if (row_max)
+            BA_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(row_max) + h0 * head_row, dM + h0 * head_row, nh * head_row,
+                                    cudaMemcpyDeviceToHost, h->stream_out));
+        if (row_sum)
+            BA_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(row_sum) + h0 * head_row, dL + h0 * head_row, nh * head_row,
+                                    cudaMemcpyDeviceToHost, h->stream_out));
+    }
+    BA_CUDA(cudaStreamSynchronize(h->stream_out));
+    BA_CUDA(cudaStreamSynchronize(h->stream));
+    BA_CUDA(cudaStreamSynchronize(h->stream_in));
     return BA_OK;
 }
 

@@ -17,7 +17,7 @@ namespace ba {
 
 constexpr int kPackThreads = 256;
 constexpr int kPackRowsPerCta = 256;
-constexpr int kPackUnroll = 4;
+constexpr int kPackUnroll = 8;
 
 struct PackJob {
     const void* X;
@@ -92,6 +92,15 @@ __device__ __forceinline__ void finish_head_sum(float acc, const PackJob& job, i
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) warp_sums[warp] = acc;
     __syncthreads();
+    if (chunks == 1) {  // the CTA saw the whole head: no cross-CTA fold, no fence, no ticket
+        if (threadIdx.x == 0 && job.mu) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < kPackThreads / 32; ++w) s += warp_sums[w];
+            job.mu[head] = (float)((double)s * inv_count);
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         float s = 0.f;
 #pragma unroll
