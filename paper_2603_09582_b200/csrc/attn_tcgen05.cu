@@ -7,23 +7,27 @@
 //                         multiplied by tcgen05.mma.kind::f8f6f4 into fp32 TMEM accumulators.  Every product is
 //                         +-1 and |sum| <= d <= 128, so the fp32 accumulator holds the integer logit exactly.
 //   x = S*mu_q*mu_k/tau + bias   (attention.cpp:34-36), softmax in the base-2 domain, fp32
-//   O += P V              bf16 tcgen05.mma.kind::f16, P staged by the softmax warps in shared memory (K-major),
-//                         V tiles brought by TMA (128B swizzle) and consumed MN-major; O accumulates in TMEM
-//   O / l                 epilogue (attention.cpp:354-364), staged in swizzled shared memory and written by TMA
+//   O += P V              bf16 tcgen05.mma.kind::f16 with the A operand (P) read straight from TENSOR MEMORY: the
+//                         softmax warps overwrite the S tile they just read with the bf16 weights (tcgen05.st), so P
+//                         never touches shared memory; V tiles come by TMA (128B swizzle), consumed MN-major
+//   O / l                 epilogue (attention.cpp:354-364): TMEM -> registers -> 32-byte vector stores
 //
-// One CTA = one (head, 128-query block); key/value tiles of 64.  256 threads:
+// PERSISTENT kernel: grid = min(units, 2 x SMs) CTAs, each walks units u = blockIdx.x, +gridDim.x, ... where one
+// unit = one (head, 128-query block); key/value tiles of 64.  All pipelines (mbarrier rings) run straight across unit
+// boundaries, so the loads, the K/Q expansion and the S MMAs of the next unit overlap the tail and the epilogue of the
+// current one, and TMEM allocation / barrier setup / the lookup table are paid once per CTA.  256 threads:
 //   warps 0-3  softmax + epilogue (thread r owns query row r == TMEM lane r)
 //   warp  4    TMEM allocation + tcgen05.mma issue (warp-uniform control flow, one elected lane issues)
 //   warp  5    TMA producer for V and bias tiles
-//   warps 6-7  K-tile expanders (bit plane -> e4m3 bytes through a shared lookup table, one key per thread)
-// Pipelines (mbarriers): K bytes 2 stages, V 2 stages, S (TMEM) 2 stages, P (smem) 1-2 stages, bias tile (bf16,
-// TMA, 128B swizzle) 1-2 stages -- the stage counts are picked on the host so that two CTAs fit one SM.  Two
-// completion barriers per tile are signalled by tcgen05.commit: sdone (S ready for the softmax warps == K stage free
-// for the expanders) and pvdone (O updated / P stage free for the softmax warps == V stage free for the TMA warp).
+//   warps 6-7  Q / K expanders (bit plane -> e4m3 bytes through a shared lookup table)
+// TMEM (256 columns): S0 [0,64) | S1 [64,128) (P aliases the first 32 columns of its S stage) | O [128,128+dvp) |
+// denominator block [128+dvp,+16).  tcgen05.mma instructions execute in issue order, and the issue order is
+// S(g+1), PV(g), S(g+2), ... so the S MMA that recycles a stage always follows the PV MMA that read P from it.
 // The running max uses the lazy-rescale rule: O/l are rescaled only when a row max grows by more than 2^8, which keeps
 // TMEM read-modify-write traffic off the common path; the final O/l is unaffected (both carry the same reference max).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "ba_common.cuh"
@@ -31,13 +35,14 @@
 namespace ba {
 namespace tc {
 
-constexpr int BM = 128;          // query rows per CTA (UMMA M)
+constexpr int BM = 128;          // query rows per unit (UMMA M)
 constexpr int BN = 64;           // keys per tile (UMMA N of the S MMA, K extent of the P.V MMA)
 constexpr int kThreads = 256;
-constexpr int kTmemCols = 256;   // S0 [0,64) | S1 [64,128) | O [128, 128+dvp) | denominator block [128+dvp, +16)
+constexpr int kTmemCols = 256;
 constexpr int kColS = 0, kColO = 128;
+constexpr int kMaxStages = 4;
+constexpr int kRegsSoftmax = 200, kRegsCtrl = 56;  // setmaxnreg split of the 2 x 128 x 128 register pool
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr uint64_t kHangNs = 4000000000ull;
 constexpr uint32_t kSuspendHint = 0x989680;  // try_wait may sleep this long before re-polling (cuts spin instructions)
 
 // ------------------------------------------------------------------------------------------------ PTX helpers
@@ -70,11 +75,11 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
         : "memory");
     return done;
 }
-// Bounded wait: a protocol bug traps after ~4 s (clean launch failure) instead of hanging the GPU.
+// Bounded wait: a protocol bug traps (clean launch failure) after 2^26 polls -- each poll sleeps in hardware up to
+// kSuspendHint ns or until the barrier moves, so that is seconds -- instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    uint64_t t0 = 0;
+    uint32_t done = 0, spins = 0;
     while (true) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -84,10 +89,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity), "r"(kSuspendHint)
             : "memory");
         if (done) break;
-        uint64_t now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > kHangNs) __trap();
+        if (++spins == (1u << 26)) __trap();
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -97,29 +99,34 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// The next three are executed by the whole MMA warp in uniform control flow (so their operands live in uniform
-// registers); `leader` predicates the instruction itself down to one lane.
-__device__ __forceinline__ void tc_commit(uint64_t* bar, uint32_t leader) {
+// One lane of a converged warp (elect.sync): the MMA warp runs its waits as a whole warp and wraps every block of
+// tcgen05.mma / tcgen05.commit instructions in `if (elect_one())`, so ptxas emits one ELECT + branch per block and the
+// operands stay in uniform registers (a per-instruction lane predicate makes it wrap each MMA in its own elect loop).
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred;
     asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
-        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
-        ::"r"(smem_u32(bar)), "r"(leader)
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, px;\n\t}"
+        : "=r"(pred));
+    return pred;
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mma_f8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc)
         : "memory");
 }
-__device__ __forceinline__ void mma_f8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc,
-                                       uint32_t leader) {
+// D[tmem] (+)= A[tmem] * B[smem]: the A operand (bf16, K-major: lane = row, one 32-bit column = two K elements).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-        "@q tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "r"(leader)
-        : "memory");
-}
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t acc,
-                                         uint32_t leader) {
-    asm volatile(
-        "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-        "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "r"(leader)
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
         : "memory");
 }
 
@@ -128,11 +135,6 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
-                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
 }
 
 // Shared-memory matrix descriptor (cute::UMMA::SmemDescriptor bit layout, mma_sm100_desc.hpp):
@@ -158,6 +160,12 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
                    "f"(v[o + 12]), "f"(v[o + 13]), "f"(v[o + 14]), "f"(v[o + 15]), "r"(taddr)                       \
                  : "memory")
 
+#define BA_TMEM_ST16U(taddr, v)                                                                                    \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15};" \
+                 ::"r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), \
+                   "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(taddr)     \
+                 : "memory")
+
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -167,6 +175,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+}
+__device__ __forceinline__ void stg_256(float* p, const float* v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]),
+                 "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
 }
 
 // 8 sign bits (bit = 1 -> +1.0) -> 8 e4m3 bytes: +1.0 = 0x38, -1.0 = 0xB8.  Used once per CTA to build the
@@ -179,22 +192,45 @@ __device__ __forceinline__ uint2 expand_byte(uint32_t b) {
 }
 
 struct Smem {
-    uint64_t kfull[2], vfull[2], sdone[2], sempty[2], pfull[2], pvdone[2], bfull[2], bempty[2];
-    uint2 lut[256];  // byte of sign bits -> 8 e4m3 +-1.0 bytes
+    uint64_t qfull[2], qfree[2];                    // Q tile expanded / every S MMA of its unit retired
+    uint64_t kfull[kMaxStages], kfree[kMaxStages];  // K tile expanded / its S MMA retired
+    uint64_t vfull[kMaxStages], vfree[kMaxStages];  // V tile landed (TMA) / its P.V MMA retired
+    uint64_t bfull[kMaxStages], bfree[kMaxStages];  // bias tile landed (TMA) / read out by the four softmax warps
+    uint64_t sfull[2];                              // S tile ready in TMEM (tcgen05.commit)
+    uint64_t pfull[2];                              // P tile written to TMEM by the four softmax warps
+    uint64_t pvdone[2];                             // P.V MMA of a tile retired (O and the denominators are up to date)
+    uint64_t ofree;                                 // O of the finished unit read out by the four softmax warps
+    uint2 lut[256];                                 // byte of sign bits -> 8 e4m3 +-1.0 bytes
     uint32_t tmem_base;
 };
+
+constexpr int kTlStamps = 256;
 
 struct Params {
     FwdArgs a;
     int mblocks;       // ceil(N / BM)
     int tiles;         // ceil(N / BN)
+    int units;         // BH * mblocks
     int dvp;           // d rounded up to 16 (UMMA N of P.V)
     int nbox;          // ceil(d / 64) TMA boxes per V tile
-    int pstages;       // P stages in shared memory (1 or 2)
-    int bstages;       // bias-tile stages (0 = no TMA bias, 1 or 2)
+    int qst, kst, vst, bst;  // ring depths in shared memory
+    int o_vec8;        // O rows are 32-byte aligned (256-bit stores)
     int32_t* dbg_S;    // optional [N,N] int32 dump of the logits of head dbg_head (tests only)
     int dbg_head;
-    long long* dbg_T;  // optional timeline: [cta][role 0..3][128] clock64 stamps (dev tool, TL kernels only)
+    long long* dbg_T;  // optional timeline: [cta][role 0..3][kTlStamps] clock64 stamps (dev tool, TL kernels only)
+};
+
+// Position in an mbarrier ring: consumers wait full[stage] with `phase`, producers wait free[stage] with phase ^ 1
+// (which passes at once on the first lap, when the barrier is still in its initial phase).
+struct Ring {
+    int stage = 0;
+    uint32_t phase = 0;
+    __device__ __forceinline__ void next(int depth) {
+        if (++stage == depth) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
 };
 
 // Packed sign words of one row -> KPAD/32 32-bit registers (zeros when !valid).
@@ -269,20 +305,20 @@ __device__ __forceinline__ float tile_max(const float (&x)[BN], int nk, int nch)
     return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
 }
 
-// p = 2^(x*ea - m_ref), rounded to bf16 and stored straight into the P stage (row `prow`, 8-key chunks 2048 B apart:
-// K-major core matrices).  SUM adds the fp32 row sum (otherwise the tensor core sums the bf16 values through the
-// ones block).  MASKED zeroes columns >= nk and stops after nch 16-column chunks.
+// p = 2^(x*ea - m_ref), rounded to bf16 and stored over the S tile just read: TMEM column c of the stage holds keys
+// 2c (low half) and 2c+1, the K-major A-operand layout of the P.V MMA.  SUM adds the fp32 row sum (otherwise the
+// tensor core sums the bf16 values through the ones block).  MASKED zeroes columns >= nk and skips the 32-key halves
+// the MMA will not read.
 template <bool MASKED, bool SUM>
-__device__ __forceinline__ float exp_store(const float (&x)[BN], int nk, int nch, float ea, float nm,
-                                           unsigned char* prow) {
+__device__ __forceinline__ float exp_store(const float (&x)[BN], int nk, int nch, float ea, float nm, uint32_t p_addr) {
     float l0 = 0.f, l1 = 0.f;
 #pragma unroll
-    for (int c = 0; c < BN / 8; ++c) {
-        if (!MASKED || c < 2 * nch) {  // (a guarded body, not a break: the loop must unroll so x[] stays in registers)
-            uint32_t pk[4];
+    for (int h = 0; h < 2; ++h) {
+        if (!MASKED || 2 * h < nch) {  // (a guarded body, not a break: the loop must unroll so x[] stays in registers)
+            uint32_t pk[16];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int i = 8 * c + 2 * e;
+            for (int e = 0; e < 16; ++e) {
+                const int i = 32 * h + 2 * e;
                 float p0 = ex2(fmaf(x[i], ea, nm));
                 float p1 = ex2(fmaf(x[i + 1], ea, nm));
                 if (MASKED) {
@@ -295,63 +331,191 @@ __device__ __forceinline__ float exp_store(const float (&x)[BN], int nk, int nch
                 }
                 pk[e] = pack_bf16(p0, p1);
             }
-            *reinterpret_cast<uint4*>(prow + c * (BM * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            BA_TMEM_ST16U(p_addr + 16 * h, pk);
         }
     }
     return l0 + l1;
 }
 
-#define BA_STAMP(role)                                                                  \
-    do {                                                                                \
-        if (TL && tl_buf && tl_n < 128) tl_buf[(role) * 128 + tl_n++] = clock64();      \
+struct RowState {
+    float m_ref, m_true, l;  // base-2 units: reference max used in the exponent, true running max, running denominator
+};
+
+// One 64-key tile of the online softmax for one query row: S (TMEM) -> x -> P (TMEM, over S).  FULL = all 64 keys valid:
+// straight-line code, every load issued up front.  The caller has waited for the S tile (and the bias stage).
+template <int BIAS, bool ROWSUM, bool FULL>
+__device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, uint32_t s_addr, uint32_t lane_base,
+                                             const unsigned char* brow, int bstage, const char* bias_row, int bias_dtype,
+                                             int j, uint32_t g, int nk, float sc, float ea, int ocols, int tid, int lane,
+                                             int32_t* dbg_row) {
+    const int nch = FULL ? BN / 16 : (nk + 15) >> 4;
+    float x[BN];
+    uint4 bv[8];
+    if (BIAS == 1 && FULL) {  // the whole bias row of the tile, issued before the TMEM loads so the latencies overlap
+#pragma unroll
+        for (int c = 0; c < 8; ++c) bv[c] = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));
+        warp_arrive(&sm->bfree[bstage], lane);
+    }
+    tc_fence_after();
+    BA_TMEM_LD16(s_addr + 0, x, 0);
+    if (FULL || nch > 1) BA_TMEM_LD16(s_addr + 16, x, 16);
+    if (FULL || nch > 2) BA_TMEM_LD16(s_addr + 32, x, 32);
+    if (FULL || nch > 3) BA_TMEM_LD16(s_addr + 48, x, 48);
+    tc_wait_ld();
+    if (dbg_row) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+            if (i < nk) dbg_row[i] = (int)x[i];
+    }
+    if (BIAS == 1 && FULL) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t bw[4] = {bv[c].x, bv[c].y, bv[c].z, bv[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc, __uint_as_float(bw[e] << 16));
+                x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc, __uint_as_float(bw[e] & 0xFFFF0000u));
+            }
+        }
+    } else if (BIAS == 1) {
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c)
+            if (c < nch) bias_chunk<1>(x, c, sc, brow, tid, nullptr, 0, 0, nk);
+        warp_arrive(&sm->bfree[bstage], lane);
+    } else if (BIAS == 2) {
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c)
+            if (c < nch) bias_chunk<2>(x, c, sc, nullptr, tid, bias_row, bias_dtype, j * BN, nk);
+    }
+    float tmax = tile_max<!FULL>(x, nk, nch);
+    tmax *= ea;  // ea >= 0, so the max commutes with the scaling
+    rs.m_true = fmaxf(rs.m_true, tmax);
+    // lazy rescale (first tile: m_ref = -inf forces it with alpha = 0 on the still-unwritten O)
+    const bool need = tmax > rs.m_ref + kRescaleThreshold;
+    if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? tmax : rs.m_ref;
+        const float alpha = need ? ex2(rs.m_ref - m_new) : 1.0f;
+        if (j > 0) {
+            mbar_wait(&sm->pvdone[(g - 1) & 1u], ((g - 1) >> 1) & 1u);  // P.V of the previous tile has landed in O
+            tc_fence_after();
+            for (int c = 0; c < ocols; c += 16) {
+                float o[16];
+                BA_TMEM_LD16(lane_base + kColO + c, o, 0);
+                tc_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[i] *= alpha;
+                BA_TMEM_ST16(lane_base + kColO + c, o, 0);
+            }
+        }
+        rs.l *= alpha;
+        rs.m_ref = m_new;
+    }
+    rs.l += exp_store<!FULL, !ROWSUM>(x, nk, nch, ea, -rs.m_ref, s_addr);
+}
+
+struct Epilogue {
+    RowState rs;
+    uint32_t g_last;  // CTA-wide index of the unit's last tile
+    int head, row;
+    bool pending, warp_ok, row_ok;
+};
+
+// O / l -> global for one finished unit, then tell the MMA warp that O may be overwritten.
+template <bool ROWSUM>
+__device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, Epilogue& ep, uint32_t lane_base, int lane) {
+    const FwdArgs& a = prm.a;
+    mbar_wait(&sm->pvdone[ep.g_last & 1u], (ep.g_last >> 1) & 1u);  // every MMA of the unit has retired
+    if (ep.warp_ok) {
+        tc_fence_after();
+        float l = ep.rs.l;
+        float* orow = a.O + ((int64_t)ep.head * a.N + ep.row) * a.d;
+        for (int c = 0; c < prm.dvp; c += 32) {
+            float o[32], den[16];
+            const bool two = c + 16 < prm.dvp;
+            if (ROWSUM && c == 0) BA_TMEM_LD16(lane_base + kColO + prm.dvp, den, 0);
+            BA_TMEM_LD16(lane_base + kColO + c, o, 0);
+            if (two) BA_TMEM_LD16(lane_base + kColO + c + 16, o, 16);
+            tc_wait_ld();
+            if (ROWSUM && c == 0) l = den[0];  // sum of the bf16 weights the MMA used (first column of the ones block)
+            const float inv_l = 1.0f / l;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= inv_l;
+            if (ep.row_ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int cc = c + 8 * q;
+                    if (cc + 8 <= a.d) {
+                        if (prm.o_vec8) {
+                            stg_256(orow + cc, o + 8 * q);
+                        } else {
+                            *reinterpret_cast<float4*>(orow + cc) = make_float4(o[8 * q], o[8 * q + 1], o[8 * q + 2], o[8 * q + 3]);
+                            *reinterpret_cast<float4*>(orow + cc + 4) = make_float4(o[8 * q + 4], o[8 * q + 5], o[8 * q + 6], o[8 * q + 7]);
+                        }
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+        if (ep.row_ok) {
+            if (a.row_max) a.row_max[(int64_t)ep.head * a.N + ep.row] = ep.rs.m_true * kLn2;
+            if (a.row_sum) a.row_sum[(int64_t)ep.head * a.N + ep.row] = l * ex2(ep.rs.m_ref - ep.rs.m_true);
+        }
+    }
+    warp_arrive(&sm->ofree, lane);
+    ep.pending = false;
+}
+
+#define BA_STAMP(role)                                                                         \
+    do {                                                                                       \
+        if (TL && tl_buf && tl_n < kTlStamps) tl_buf[(role) * kTlStamps + tl_n++] = clock64(); \
     } while (0)
 
 // BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
 template <int KPAD, int BIAS, bool TL = false>
 __global__ void __launch_bounds__(kThreads, 2)
 attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap,
-               const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap) {
+               const __grid_constant__ CUtensorMap bmap) {
     // d <= 96 leaves 16 spare TMEM columns next to O: the softmax denominator is then accumulated by the tensor
     // core (P x ones), which removes one FADD per score from the softmax warps.
     constexpr bool ROWSUM = KPAD <= 96;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
-    // carve shared memory: V stages | bias stages | P stages (1024-aligned; the O staging of the epilogue reuses this
-    // region once every MMA has retired) | Q tile | K stages | ones | barriers + table
-    unsigned char* sV = smem_raw;                                   // 2 x nbox x 8192
-    unsigned char* sB = sV + 2 * prm.nbox * 8192;                   // bstages x 16384
-    unsigned char* sP = sB + prm.bstages * 16384;                   // pstages x 16384
-    unsigned char* sQ = sP + prm.pstages * 16384;                   // BM x KPAD
-    unsigned char* sK = sQ + BM * KPAD;                             // 2 x BN x KPAD
-    unsigned char* sOnes = sK + 2 * BN * KPAD;                      // 512 B of bf16 1.0 (B operand of the row-sum MMA)
+    // carve shared memory: V ring | bias ring (both 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
+    unsigned char* sV = smem_raw;                                   // vst x nbox x 8192
+    unsigned char* sB = sV + prm.vst * prm.nbox * 8192;             // bst x 16384
+    unsigned char* sQ = sB + prm.bst * 16384;                       // qst x BM x KPAD
+    unsigned char* sK = sQ + prm.qst * BM * KPAD;                   // kst x BN x KPAD
+    unsigned char* sOnes = sK + prm.kst * BN * KPAD;                // 512 B of bf16 1.0 (B operand of the row-sum MMA)
     Smem* sm = reinterpret_cast<Smem*>(sOnes + 512);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int head = blockIdx.x / prm.mblocks;
-    const int mb = blockIdx.x - head * prm.mblocks;
     const int N = a.N, d = a.d, w64 = a.W64, T = prm.tiles;
-    const int row0 = mb * BM;
-    const int pst = prm.pstages;
-    const bool b2 = prm.bstages == 2;
+    const int G = gridDim.x;
     const int ocols = prm.dvp + (ROWSUM ? 16 : 0);  // TMEM columns of the O accumulator (+ denominator block)
-    long long* tl_buf = (TL && prm.dbg_T) ? prm.dbg_T + (size_t)blockIdx.x * 4 * 128 : nullptr;
+    long long* tl_buf = (TL && prm.dbg_T) ? prm.dbg_T + (size_t)blockIdx.x * 4 * kTlStamps : nullptr;
     int tl_n = 0;
     (void)tl_buf; (void)tl_n;
     if (TL && !(tid == 0 || tid == 128 || tid == 160 || tid == 192)) tl_buf = nullptr;  // one stamper per role
     BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
 
-    // ---------------------------------------------------------------- prologue
+    // ---------------------------------------------------------------- prologue (once per CTA)
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm->kfull[s], 2);     // one elected arrival per expander warp
-            mbar_init(&sm->vfull[s], 1);     // expect_tx arrive + TMA bytes
-            mbar_init(&sm->sdone[s], 1);     // tcgen05.commit after the S MMA of a tile
-            mbar_init(&sm->sempty[s], 4);    // one elected arrival per softmax warp (S stage read out)
-            mbar_init(&sm->pfull[s], 4);     // one elected arrival per softmax warp (P stage written)
+            mbar_init(&sm->qfull[s], 2);     // one elected arrival per expander warp
+            mbar_init(&sm->qfree[s], 1);     // tcgen05.commit after the last S MMA of the unit
+            mbar_init(&sm->sfull[s], 1);     // tcgen05.commit after the S MMA of a tile
+            mbar_init(&sm->pfull[s], 4);     // one elected arrival per softmax warp (P tile written to TMEM)
             mbar_init(&sm->pvdone[s], 1);    // tcgen05.commit after the P.V MMA of a tile
-            mbar_init(&sm->bfull[s], 1);     // expect_tx arrive + TMA bytes
-            mbar_init(&sm->bempty[s], 4);    // one elected arrival per softmax warp (bias stage read out)
         }
+        for (int s = 0; s < kMaxStages; ++s) {
+            mbar_init(&sm->kfull[s], 2);     // one elected arrival per expander warp
+            mbar_init(&sm->kfree[s], 1);     // tcgen05.commit after the S MMA that read the stage
+            mbar_init(&sm->vfull[s], 1);     // expect_tx arrive + TMA bytes
+            mbar_init(&sm->vfree[s], 1);     // tcgen05.commit after the P.V MMA that read the stage
+            mbar_init(&sm->bfull[s], 1);     // expect_tx arrive + TMA bytes
+            mbar_init(&sm->bfree[s], 4);     // one elected arrival per softmax warp (bias stage read out)
+        }
+        mbar_init(&sm->ofree, 4);            // one elected arrival per softmax warp (O read out by the epilogue)
         fence_barrier_init();
     }
     if (warp == 4) {
@@ -362,29 +526,22 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     }
     if (warp == 5 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&omap)) : "memory");
         if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
     }
     sm->lut[tid] = expand_byte((uint32_t)tid);
     if (tid < 128) reinterpret_cast<uint32_t*>(sOnes)[tid] = 0x3F803F80u;  // bf16 1.0 pairs
-    // the first packed words are fetched before the barrier so their latency overlaps the table build
-    uint32_t w32[KPAD / 32];
-    if (tid < BM) load_words<KPAD>(w32, a.q_words + ((int64_t)head * N + row0 + tid) * w64, w64, row0 + tid < N);
-    else if (warp >= 6) load_words<KPAD>(w32, a.k_words + ((int64_t)head * N + (tid - 192)) * w64, w64, tid - 192 < N);
-    float sc = 0.f;
-    if (tid < BM) sc = __ldg(a.mu_q + head) * __ldg(a.mu_k + head) * a.inv_tau;  // natural-log units per unit of dot
-    __syncthreads();
-    if (tid < BM) expand_store<KPAD>(sQ, BM, tid, w32, d, row0 + tid < N, sm->lut);  // Q tile: thread r = query row
-    fence_proxy_async();
+    fence_proxy_async();  // the ones block is read by the tensor core (async proxy)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm->tmem_base;
     BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
-
+    // register rebalancing between the two warpgroups (the pool is 256 x 128 per CTA): the softmax threads hold a
+    // 64-column score row plus the bias row, the control warps need very little
+    if (warp >= 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtrl));
     if (warp == 4) {
         // ============================================================ MMA issuer (whole warp, uniform control flow)
-        const uint32_t leader = lane == 0 ? 1u : 0u;
         // instruction descriptors (cute::UMMA::InstrDescriptor bit layout)
         const uint32_t idesc_s = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);  // e4m3 x e4m3 -> f32, K-major A/B
         const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |                      // bf16 x bf16 -> f32, B MN-major
@@ -393,230 +550,232 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                                  ((uint32_t)(BM >> 4) << 24);
         const uint64_t q_desc = make_desc(smem_u32(sQ), BM * 16, 128, 0);     // K-major no swizzle; +ks*2*BM*16 per K step
         const uint64_t k_desc = make_desc(smem_u32(sK), BN * 16, 128, 0);     // +s*BN*KPAD per stage, +ks*2*BN*16 per K step
-        const uint64_t p_desc = make_desc(smem_u32(sP), 2048, 128, 0);        // +ps*16384 per stage, +ks*4096 per K step
         const uint64_t v_desc = make_desc(smem_u32(sV), 8192, 1024, 2);       // MN-major 128B swizzle; +ks*2048 per 16 keys
         const uint64_t ones_desc = make_desc(smem_u32(sOnes), 256, 128, 0);   // 16 x 16 block of ones: any layout reads 1.0
-        auto issue_pv = [&](int t) {
-            const int s = t & 1, n = t >> 1;
-            const int ps = pst == 2 ? s : 0, pn = pst == 2 ? n : t;
-            const uint32_t v_ok = mbar_try(&sm->vfull[s], n & 1);
-            mbar_wait(&sm->pfull[ps], pn & 1);
-            if (!v_ok) mbar_wait(&sm->vfull[s], n & 1);
+        Ring qr, kr, vr;
+        uint32_t g = 0;  // tiles issued so far by this CTA (S stage = g & 1)
+        // the P.V MMA of a tile is issued one tile late, after the S MMA of the next tile (also across unit boundaries)
+        int pend = 0, pend_nk = 0, pend_j = 0, pend_unit = 0;
+        uint32_t pend_g = 0;
+        auto issue_pv = [&]() {
+            const uint32_t s = pend_g & 1u;
+            const uint32_t v_ok = mbar_try(&sm->vfull[vr.stage], vr.phase);
+            mbar_wait(&sm->pfull[s], (pend_g >> 1) & 1u);
+            if (!v_ok) mbar_wait(&sm->vfull[vr.stage], vr.phase);
+            // the first tile of a unit overwrites O: the epilogue of the previous unit must have read it out
+            if (pend_j == 0 && pend_unit > 0) mbar_wait(&sm->ofree, (uint32_t)(pend_unit - 1) & 1u);
             BA_STAMP(1);
             tc_fence_after();
-            const int nk = min(BN, N - t * BN);
-            const int ksteps = (nk + 15) >> 4;
-            const uint64_t pd = p_desc + (uint64_t)((ps * 16384) >> 4);
-            const uint64_t vd = v_desc + (uint64_t)((s * prm.nbox * 8192) >> 4);
-            for (int ks = 0; ks < ksteps; ++ks) {
-                const uint32_t acc = (t > 0 || ks > 0) ? 1u : 0u;
-                mma_bf16(tmem + kColO, pd + (uint64_t)(ks * (4096 >> 4)), vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv, acc, leader);
-                if (ROWSUM) mma_bf16(tmem + kColO + prm.dvp, pd + (uint64_t)(ks * (4096 >> 4)), ones_desc, idesc_l, acc, leader);
+            const int ksteps = (pend_nk + 15) >> 4;
+            const uint32_t p_tmem = tmem + kColS + s * BN;
+            const uint64_t vd = v_desc + (uint64_t)((vr.stage * prm.nbox * 8192) >> 4);
+            if (elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < BN / 16; ++ks) {
+                    if (ks < ksteps) {
+                        const uint32_t acc = (pend_j > 0 || ks > 0) ? 1u : 0u;
+                        mma_bf16_ts(tmem + kColO, p_tmem + ks * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv, acc);
+                        if (ROWSUM) mma_bf16_ts(tmem + kColO + prm.dvp, p_tmem + ks * 8, ones_desc, idesc_l, acc);
+                    }
+                }
+                tc_commit(&sm->pvdone[s]);
+                tc_commit(&sm->vfree[vr.stage]);
             }
-            tc_commit(&sm->pvdone[s], leader);
+            __syncwarp();
+            vr.next(prm.vst);
             BA_STAMP(1);
         };
-        for (int j = 0; j < T; ++j) {
-            const int s = j & 1, n = j >> 1;
-            const uint32_t s_ok = n > 0 ? mbar_try(&sm->sempty[s], (n & 1) ^ 1) : 1u;  // first use: stage is free
-            mbar_wait(&sm->kfull[s], n & 1);
-            if (!s_ok) mbar_wait(&sm->sempty[s], (n & 1) ^ 1);
-            BA_STAMP(1);
-            tc_fence_after();
-            const uint64_t kd = k_desc + (uint64_t)((s * BN * KPAD) >> 4);
+        int unit_i = 0;
+        for (int u = blockIdx.x; u < prm.units; u += G, ++unit_i) {
+            mbar_wait(&sm->qfull[qr.stage], qr.phase);
+            const uint64_t qd = q_desc + (uint64_t)((qr.stage * BM * KPAD) >> 4);
+            for (int j = 0; j < T; ++j) {
+                mbar_wait(&sm->kfull[kr.stage], kr.phase);
+                BA_STAMP(1);
+                tc_fence_after();
+                const uint64_t kd = k_desc + (uint64_t)((kr.stage * BN * KPAD) >> 4);
+                if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < KPAD / 32; ++ks)
-                mma_f8(tmem + kColS + s * BN, q_desc + (uint64_t)(ks * ((2 * BM * 16) >> 4)),
-                       kd + (uint64_t)(ks * ((2 * BN * 16) >> 4)), idesc_s, ks > 0 ? 1u : 0u, leader);
-            tc_commit(&sm->sdone[s], leader);
-            BA_STAMP(1);
-            if (j > 0) issue_pv(j - 1);
+                    for (int ks = 0; ks < KPAD / 32; ++ks)
+                        mma_f8(tmem + kColS + (g & 1u) * BN, qd + (uint64_t)(ks * ((2 * BM * 16) >> 4)),
+                               kd + (uint64_t)(ks * ((2 * BN * 16) >> 4)), idesc_s, ks > 0 ? 1u : 0u);
+                    tc_commit(&sm->sfull[g & 1u]);
+                    tc_commit(&sm->kfree[kr.stage]);
+                    if (j == T - 1) tc_commit(&sm->qfree[qr.stage]);
+                }
+                __syncwarp();
+                kr.next(prm.kst);
+                BA_STAMP(1);
+                if (pend) issue_pv();
+                pend = 1;
+                pend_g = g;
+                pend_j = j;
+                pend_unit = unit_i;
+                pend_nk = min(BN, N - j * BN);
+                ++g;
+            }
+            qr.next(prm.qst);
         }
-        issue_pv(T - 1);
+        if (pend) issue_pv();
     } else if (warp == 5) {
         // ============================================================ TMA producer (V tiles, bias tiles)
         if (lane == 0) {
-            const int bh = (a.head0 + head) % a.H % a.bias_heads;
-            for (int j = 0; j < T; ++j) {
-                const int s = j & 1, n = j >> 1;
-                if (BIAS == 1) {
-                    const int bs = b2 ? s : 0, bn = b2 ? n : j;
-                    if (bn > 0) mbar_wait(&sm->bempty[bs], (bn & 1) ^ 1);
-                    mbar_expect_tx(&sm->bfull[bs], 16384);
-                    tma_load_3d(&bmap, &sm->bfull[bs], sB + bs * 16384, j * BN, row0, bh);
+            Ring vr, br;
+            for (int u = blockIdx.x; u < prm.units; u += G) {
+                const int head = u / prm.mblocks;
+                const int row0 = (u - head * prm.mblocks) * BM;
+                const int bh = (a.head0 + head) % a.H % a.bias_heads;
+                for (int j = 0; j < T; ++j) {
+                    if (BIAS == 1) {
+                        mbar_wait(&sm->bfree[br.stage], br.phase ^ 1u);
+                        mbar_expect_tx(&sm->bfull[br.stage], 16384);
+                        tma_load_3d(&bmap, &sm->bfull[br.stage], sB + br.stage * 16384, j * BN, row0, bh);
+                        br.next(prm.bst);
+                    }
+                    BA_STAMP(2);
+                    mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
+                    BA_STAMP(2);
+                    mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * 8192);
+                    for (int b = 0; b < prm.nbox; ++b)
+                        tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * 8192, b * 64, j * BN, head);
+                    vr.next(prm.vst);
                 }
-                BA_STAMP(2);
-                if (n > 0) mbar_wait(&sm->pvdone[s], (n & 1) ^ 1);  // P.V of tile j-2 released this V stage
-                BA_STAMP(2);
-                mbar_expect_tx(&sm->vfull[s], prm.nbox * 8192);
-                for (int b = 0; b < prm.nbox; ++b)
-                    tma_load_3d(&vmap, &sm->vfull[s], sV + (s * prm.nbox + b) * 8192, b * 64, j * BN, head);
             }
         }
     } else if (warp >= 6) {
-        // ============================================================ K expanders (one key per thread)
-        const int t = tid - 6 * 32;
-        for (int j = 0; j < T; ++j) {
-            const int s = j & 1, n = j >> 1;
-            const int key = j * BN + t;
-            if (n > 0) mbar_wait(&sm->sdone[s], (n & 1) ^ 1);  // S MMA of tile j-2 released this K stage
-            BA_STAMP(3);
-            expand_store<KPAD>(sK + s * BN * KPAD, BN, t, w32, d, key < N, sm->lut);
-            BA_STAMP(3);
-            fence_proxy_async();
-            warp_arrive(&sm->kfull[s], lane);
-            BA_STAMP(3);
-            // prefetch the next tile's words so their L2 latency hides behind the next wait
-            if (j + 1 < T) load_words<KPAD>(w32, a.k_words + ((int64_t)head * N + key + BN) * w64, w64, key + BN < N);
+        // ============================================================ Q / K expanders
+        const int t = tid - 6 * 32;  // 0..63: key t of every K tile, query rows t and t + 64 of every Q tile
+        Ring qr, kr;
+        uint32_t wq0[KPAD / 32], wq1[KPAD / 32], wk[KPAD / 32];
+        if ((int)blockIdx.x < prm.units) {  // words of the first unit
+            const int head = blockIdx.x / prm.mblocks;
+            const int row0 = (blockIdx.x - head * prm.mblocks) * BM;
+            load_words<KPAD>(wq0, a.q_words + ((int64_t)head * N + row0 + t) * w64, w64, row0 + t < N);
+            load_words<KPAD>(wq1, a.q_words + ((int64_t)head * N + row0 + t + 64) * w64, w64, row0 + t + 64 < N);
+            load_words<KPAD>(wk, a.k_words + ((int64_t)head * N + t) * w64, w64, t < N);
         }
+        for (int u = blockIdx.x; u < prm.units; u += G) {
+            const int head = u / prm.mblocks;
+            const int row0 = (u - head * prm.mblocks) * BM;
+            mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
+            unsigned char* qt = sQ + qr.stage * BM * KPAD;
+            expand_store<KPAD>(qt, BM, t, wq0, d, row0 + t < N, sm->lut);
+            expand_store<KPAD>(qt, BM, t + 64, wq1, d, row0 + t + 64 < N, sm->lut);
+            fence_proxy_async();
+            warp_arrive(&sm->qfull[qr.stage], lane);
+            qr.next(prm.qst);
+            // Q words of the next unit: their latency hides behind this unit's K tiles
+            const int un = u + G;
+            const int hn = un / prm.mblocks;
+            if (un < prm.units) {
+                const int rn = (un - hn * prm.mblocks) * BM;
+                load_words<KPAD>(wq0, a.q_words + ((int64_t)hn * N + rn + t) * w64, w64, rn + t < N);
+                load_words<KPAD>(wq1, a.q_words + ((int64_t)hn * N + rn + t + 64) * w64, w64, rn + t + 64 < N);
+            }
+            for (int j = 0; j < T; ++j) {
+                const int key = j * BN + t;
+                mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
+                BA_STAMP(3);
+                expand_store<KPAD>(sK + kr.stage * BN * KPAD, BN, t, wk, d, key < N, sm->lut);
+                fence_proxy_async();
+                warp_arrive(&sm->kfull[kr.stage], lane);
+                kr.next(prm.kst);
+                BA_STAMP(3);
+                // prefetch the next tile's words (the next unit's first tile after the last one)
+                if (j + 1 < T) load_words<KPAD>(wk, a.k_words + ((int64_t)head * N + key + BN) * w64, w64, key + BN < N);
+                else if (un < prm.units) load_words<KPAD>(wk, a.k_words + ((int64_t)hn * N + t) * w64, w64, t < N);
+            }
+        }
+    }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
         // ============================================================ softmax + epilogue (thread = query row)
-        const int row = row0 + tid;
-        const bool row_ok = row < N;
-        const bool warp_ok = row0 + warp * 32 < N;  // warps whose 32 rows are all past N only keep the barriers moving
         const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-        // BIAS == 0 keeps x = raw integer dot and folds sc*log2e into the exponent FMA; otherwise x = dot*sc + bias
-        const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;
-        const char* bias_row = nullptr;
-        if (BIAS == 2 && row_ok)
-            bias_row = static_cast<const char*>(a.bias) +
-                       ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
-        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.f;  // base-2 units
-        uint32_t s_ok = mbar_try(&sm->sdone[0], 0);
+        Ring br;
+        uint32_t g = 0;  // tiles consumed so far (S stage = g & 1)
+        float sc_next = 0.f;
+        if ((int)blockIdx.x < prm.units) {
+            const int head = blockIdx.x / prm.mblocks;
+            sc_next = __ldg(a.mu_q + head) * __ldg(a.mu_k + head) * a.inv_tau;
+        }
+        // The epilogue of a unit is deferred until the first tile of the NEXT unit has been through the softmax, so the
+        // latency of the unit's last P.V MMA hides behind useful work (the MMA warp holds that next tile's P.V back until
+        // `ofree` says O has been read out).
+        Epilogue ep{};
+        ep.pending = false;
+        uint32_t s_ok = mbar_try(&sm->sfull[0], 0);
+        for (int u = blockIdx.x; u < prm.units; u += G) {
+            const int head = u / prm.mblocks;
+            const int row0 = (u - head * prm.mblocks) * BM;
+            const int row = row0 + tid;
+            const bool row_ok = row < N;
+            const bool warp_ok = row0 + warp * 32 < N;  // warps whose 32 rows are all past N only keep the barriers moving
+            const float sc = sc_next;  // natural-log units per unit of dot
+            if (u + G < prm.units) {
+                const int hn = (u + G) / prm.mblocks;
+                sc_next = __ldg(a.mu_q + hn) * __ldg(a.mu_k + hn) * a.inv_tau;
+            }
+            // BIAS == 0 keeps x = raw integer dot and folds sc*log2e into the exponent FMA; otherwise x = dot*sc + bias
+            const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;
+            const char* bias_row = nullptr;
+            if (BIAS == 2 && row_ok)
+                bias_row = static_cast<const char*>(a.bias) +
+                           ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+            RowState rs{-INFINITY, -INFINITY, 0.f};
+            const bool dump = prm.dbg_S && head == prm.dbg_head && row_ok;
 
-        for (int j = 0; j < T; ++j) {
-            const int s = j & 1, n = j >> 1;
-            const int ps = pst == 2 ? s : 0;
-            const int bs = b2 ? s : 0, bn = b2 ? n : j;
-            const int nk = min(BN, N - j * BN);
-            const int nch = (nk + 15) >> 4;
-            // "P stage free" = P.V of tile j-pstages retired (always true for the first pstages tiles)
-            const int jf = j - pst;
-            BA_STAMP(0);
-            if (!s_ok) mbar_wait(&sm->sdone[s], n & 1);
-            BA_STAMP(0);
-            if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
-                warp_arrive(&sm->sempty[s], lane);
-                if (BIAS == 1) {
-                    mbar_wait(&sm->bfull[bs], bn & 1);
-                    warp_arrive(&sm->bempty[bs], lane);
-                }
-                if (jf >= 0) mbar_wait(&sm->pvdone[jf & 1], (jf >> 1) & 1);
-                warp_arrive(&sm->pfull[ps], lane);
-                s_ok = (j + 1 < T) ? mbar_try(&sm->sdone[s ^ 1], ((j + 1) >> 1) & 1) : 1u;
-                continue;
-            }
-            float x[BN];
-            tc_fence_after();
-            const uint32_t s_addr = lane_base + kColS + s * BN;
-            BA_TMEM_LD16(s_addr + 0, x, 0);
-            if (nch > 1) BA_TMEM_LD16(s_addr + 16, x, 16);
-            if (nch > 2) BA_TMEM_LD16(s_addr + 32, x, 32);
-            if (nch > 3) BA_TMEM_LD16(s_addr + 48, x, 48);
-            uint32_t b_ok = 1;
-            if (BIAS == 1) b_ok = mbar_try(&sm->bfull[bs], bn & 1);  // these polls overlap the TMEM load
-            const uint32_t p_ok = jf >= 0 ? mbar_try(&sm->pvdone[jf & 1], (jf >> 1) & 1) : 1u;
-            tc_wait_ld();
-            tc_fence_before();
-            warp_arrive(&sm->sempty[s], lane);
-            BA_STAMP(0);
-
-            if (prm.dbg_S && head == prm.dbg_head && row_ok) {
-#pragma unroll
-                for (int i = 0; i < BN; ++i)
-                    if (i < nk) prm.dbg_S[(int64_t)row * N + j * BN + i] = (int)x[i];
-            }
-            if (BIAS == 1) {
-                if (!b_ok) mbar_wait(&sm->bfull[bs], bn & 1);
-                const unsigned char* brow = sB + bs * 16384 + tid * 128;  // row tid of the 128 x 64 bf16 tile
-#pragma unroll
-                for (int c = 0; c < BN / 16; ++c)
-                    if (c < nch) bias_chunk<1>(x, c, sc, brow, tid, nullptr, 0, 0, nk);
-                warp_arrive(&sm->bempty[bs], lane);
-            } else if (BIAS == 2) {
-#pragma unroll
-                for (int c = 0; c < BN / 16; ++c)
-                    if (c < nch) bias_chunk<2>(x, c, sc, nullptr, tid, bias_row, a.bias_dtype, j * BN, nk);
-            }
-            BA_STAMP(0);
-            float tmax = (nk == BN) ? tile_max<false>(x, nk, nch) : tile_max<true>(x, nk, nch);
-            tmax *= ea;  // ea >= 0, so the max commutes with the scaling
-            m_true = fmaxf(m_true, tmax);
-            // lazy rescale (first tile: m_ref = -inf forces it with alpha = 0 on the still-unwritten O)
-            const bool need = tmax > m_ref + kRescaleThreshold;
-            if (__any_sync(0xffffffffu, need)) {
-                const float m_new = need ? tmax : m_ref;
-                const float alpha = need ? ex2(m_ref - m_new) : 1.0f;
-                if (j > 0) {
-                    mbar_wait(&sm->pvdone[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P.V of tile j-1 has landed in O
-                    tc_fence_after();
-                    for (int c = 0; c < ocols; c += 16) {
-                        float o[16];
-                        BA_TMEM_LD16(lane_base + kColO + c, o, 0);
-                        tc_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) o[i] *= alpha;
-                        BA_TMEM_ST16(lane_base + kColO + c, o, 0);
+            for (int j = 0; j < T; ++j, ++g) {
+                const uint32_t s = g & 1u;
+                const int nk = min(BN, N - j * BN);
+                BA_STAMP(0);
+                if (!s_ok) mbar_wait(&sm->sfull[s], (g >> 1) & 1u);
+                BA_STAMP(0);
+                if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
+                    if (BIAS == 1) {
+                        mbar_wait(&sm->bfull[br.stage], br.phase);
+                        warp_arrive(&sm->bfree[br.stage], lane);
+                        br.next(prm.bst);
                     }
+                    warp_arrive(&sm->pfull[s], lane);
+                } else {
+                    const unsigned char* brow = nullptr;
+                    if (BIAS == 1) {
+                        mbar_wait(&sm->bfull[br.stage], br.phase);
+                        brow = sB + br.stage * 16384 + tid * 128;  // row tid of the 128 x 64 bf16 tile
+                    }
+                    const uint32_t s_addr = lane_base + kColS + s * BN;
+                    int32_t* dbg_row = dump ? prm.dbg_S + (int64_t)row * N + j * BN : nullptr;
+                    if (nk == BN)
+                        softmax_tile<BIAS, ROWSUM, true>(sm, rs, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g, nk,
+                                                         sc, ea, ocols, tid, lane, dbg_row);
+                    else
+                        softmax_tile<BIAS, ROWSUM, false>(sm, rs, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g, nk,
+                                                          sc, ea, ocols, tid, lane, dbg_row);
+                    if (BIAS == 1) br.next(prm.bst);
                     tc_wait_st();
                     tc_fence_before();
+                    warp_arrive(&sm->pfull[s], lane);
                 }
-                l *= alpha;
-                m_ref = m_new;
-            }
-            if (!p_ok) mbar_wait(&sm->pvdone[jf & 1], (jf >> 1) & 1);  // the previous P.V on this stage no longer reads it
-            BA_STAMP(0);
-            unsigned char* prow = sP + ps * 16384 + tid * 16;
-            if (nk == BN) l += exp_store<false, !ROWSUM>(x, nk, nch, ea, -m_ref, prow);
-            else l += exp_store<true, !ROWSUM>(x, nk, nch, ea, -m_ref, prow);
-            BA_STAMP(0);
-            fence_proxy_async();
-            warp_arrive(&sm->pfull[ps], lane);
-            s_ok = (j + 1 < T) ? mbar_try(&sm->sdone[s ^ 1], ((j + 1) >> 1) & 1) : 1u;
-            BA_STAMP(0);
-        }
-        // ---------------------------------------------------------------- epilogue: O / l -> swizzled smem -> TMA store
-        mbar_wait(&sm->pvdone[(T - 1) & 1], ((T - 1) >> 1) & 1);  // every MMA has retired: all tile smem is free
-        BA_STAMP(0);
-        if (warp_ok) {
-            tc_fence_after();
-            if (ROWSUM) {  // denominator = first column of the ones block (sum of the bf16 weights the MMA used)
-                float o[16];
-                BA_TMEM_LD16(lane_base + kColO + prm.dvp, o, 0);
-                tc_wait_ld();
-                l = o[0];
-            }
-            const float inv_l = 1.0f / l;
-            // staging: per warp, boxes of [32 rows][32 floats] = 4 KB, 128B-swizzled like the O tensor map
-            const int nobox = (d + 31) >> 5;
-            unsigned char* stage = smem_raw + warp * nobox * 4096;
-            for (int c = 0; c < prm.dvp; c += 16) {
-                float o[16];
-                BA_TMEM_LD16(lane_base + kColO + c, o, 0);
-                tc_wait_ld();
-                unsigned char* box = stage + (c >> 5) * 4096 + lane * 128;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int chunk = ((c & 16) >> 2) + q;  // 16-byte chunk inside the 128-byte box row
-                    *reinterpret_cast<float4*>(box + ((chunk ^ (lane & 7)) << 4)) =
-                        make_float4(o[4 * q] * inv_l, o[4 * q + 1] * inv_l, o[4 * q + 2] * inv_l, o[4 * q + 3] * inv_l);
+                // poll the next S tile now: the answer arrives while the deferred epilogue / loop overhead runs
+                s_ok = mbar_try(&sm->sfull[s ^ 1u], ((g + 1) >> 1) & 1u);
+                BA_STAMP(0);
+                if (j == 0 && ep.pending) {
+                    run_epilogue<ROWSUM>(sm, prm, ep, lane_base, lane);
+                    BA_STAMP(0);
                 }
             }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                for (int b = 0; b < nobox; ++b) tma_store_3d(&omap, stage + b * 4096, b * 32, row0 + warp * 32, head);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-            if (row_ok) {
-                if (a.row_max) a.row_max[(int64_t)head * N + row] = m_true * kLn2;
-                if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l * ex2(m_ref - m_true);
-            }
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem may be released
-            tc_fence_before();
+            ep.pending = true;
+            ep.warp_ok = warp_ok;
+            ep.row_ok = row_ok;
+            ep.head = head;
+            ep.row = row;
+            ep.g_last = g - 1;
+            ep.rs = rs;
         }
+        if (ep.pending) run_epilogue<ROWSUM>(sm, prm, ep, lane_base, lane);
         BA_STAMP(0);
     }
+    tc_fence_before();
     __syncthreads();
     BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
     if (warp == 4) {
@@ -645,42 +804,44 @@ static EncodeTiledFn get_encode() {
 static int32_t* g_dbg_S = nullptr;
 static int g_dbg_head = -1;
 static long long* g_dbg_T = nullptr;
-constexpr size_t kSmemBudget = 113 * 1024;
-constexpr size_t kSmemMax = 227 * 1024;  // two CTAs per SM (227 KB usable, 1 KB reserved per CTA)
+constexpr size_t kSmemBudget = 113 * 1024;  // two CTAs per SM (227 KB usable, 1 KB reserved per CTA)
 
-static size_t smem_pad() {  // dev knob: BA_SMEM_PAD=<bytes> forces lower occupancy for experiments
-    static long pad = -1;
-    if (pad < 0) { const char* e = getenv("BA_SMEM_PAD"); pad = e ? atol(e) : 0; }
-    return (size_t)pad;
+static long env_long(const char* name, long dflt) {
+    const char* e = getenv(name);
+    return e ? atol(e) : dflt;
 }
 static size_t smem_bytes(const Params& prm, int kpad) {
-    return smem_pad() + 2 * (size_t)prm.nbox * 8192 + (size_t)prm.bstages * 16384 + (size_t)prm.pstages * 16384 + (size_t)BM * kpad +
-           2 * (size_t)BN * kpad + 512 + sizeof(Smem);
+    return (size_t)prm.vst * prm.nbox * 8192 + (size_t)prm.bst * 16384 + (size_t)prm.qst * BM * kpad +
+           (size_t)prm.kst * BN * kpad + 512 + sizeof(Smem);
 }
 
 struct Maps {
-    CUtensorMap v, b, o;
+    CUtensorMap v, b;
 };
 
-template <int KPAD, int BIAS>
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int KPAD, int BIAS, bool TL>
 static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)kSmemMax);
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)kSmemBudget);
         if (e != cudaSuccess) return -(int)e;
         configured = true;
     }
-    attn_tc_kernel<KPAD, BIAS><<<(unsigned)(prm.a.BH * prm.mblocks), kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o);
-    const cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 1 : -(int)e;
-}
-
-// Timeline build of three representative variants (dev tool; selected when a timeline buffer is registered).
-template <int KPAD, int BIAS>
-static int launch_timeline(const Params& prm, const Maps& m, cudaStream_t stream) {
-    cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-    attn_tc_kernel<KPAD, BIAS, true><<<(unsigned)(prm.a.BH * prm.mblocks), kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o);
+    const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
+    const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
+    attn_tc_kernel<KPAD, BIAS, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
@@ -688,9 +849,9 @@ static int launch_timeline(const Params& prm, const Maps& m, cudaStream_t stream
 template <int KPAD>
 static int launch_kpad(const Params& prm, int bias_mode, const Maps& m, cudaStream_t stream) {
     switch (bias_mode) {
-        case 0: return launch_variant<KPAD, 0>(prm, m, stream);
-        case 1: return launch_variant<KPAD, 1>(prm, m, stream);
-        default: return launch_variant<KPAD, 2>(prm, m, stream);
+        case 0: return launch_variant<KPAD, 0, false>(prm, m, stream);
+        case 1: return launch_variant<KPAD, 1, false>(prm, m, stream);
+        default: return launch_variant<KPAD, 2, false>(prm, m, stream);
     }
 }
 
@@ -716,8 +877,10 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.a = a;
     prm.mblocks = (a.N + BM - 1) / BM;
     prm.tiles = (a.N + BN - 1) / BN;
+    prm.units = a.BH * prm.mblocks;
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
+    prm.o_vec8 = reinterpret_cast<uintptr_t>(a.O) % 32 == 0 ? 1 : 0;  // d % 8 == 0 keeps every row 32-byte aligned
     prm.dbg_S = g_dbg_S;
     prm.dbg_head = g_dbg_head;
     prm.dbg_T = g_dbg_T;
@@ -730,11 +893,16 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                             reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         bias_mode = tma_ok ? 1 : 2;
     }
-    // stage counts: as deep as fits two CTAs per SM
-    prm.pstages = 2;
-    prm.bstages = bias_mode == 1 ? 2 : 0;
-    if (smem_bytes(prm, kpad) > kSmemBudget) prm.pstages = 1;
-    if (smem_bytes(prm, kpad) > kSmemBudget && prm.bstages == 2) prm.bstages = 1;
+    // ring depths: as deep as fits two CTAs per SM
+    prm.qst = 2;
+    prm.kst = 3;
+    prm.vst = 3;
+    prm.bst = bias_mode == 1 ? 2 : 0;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.qst = 1;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.kst = 2;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.vst = 2;
+    if (smem_bytes(prm, kpad) > kSmemBudget && prm.bst == 2) prm.bst = 1;
+    if (smem_bytes(prm, kpad) > kSmemBudget) return -(int)cudaErrorInvalidConfiguration;
 
     Maps m;
     const cuuint32_t estr[3] = {1, 1, 1};
@@ -747,14 +915,6 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
-    {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 32 floats (128 B), clipped at N and d by the hardware
-        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
-        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
-        const cuuint32_t box[3] = {32, 32, 1};
-        if (enc(&m.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return -(int)cudaErrorInvalidValue;
-    }
     m.b = m.v;
     if (bias_mode == 1) {
         const cuuint64_t gdim[3] = {(cuuint64_t)a.N, (cuuint64_t)a.N, (cuuint64_t)a.bias_heads};
@@ -765,10 +925,10 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
-    if (g_dbg_T) {
-        if (kpad == 64 && bias_mode == 1) return launch_timeline<64, 1>(prm, m, stream);
-        if (kpad == 64 && bias_mode == 0) return launch_timeline<64, 0>(prm, m, stream);
-        if (kpad == 128 && bias_mode == 0) return launch_timeline<128, 0>(prm, m, stream);
+    if (g_dbg_T) {  // timeline build of three representative variants (dev tool)
+        if (kpad == 64 && bias_mode == 1) return launch_variant<64, 1, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 0) return launch_variant<64, 0, true>(prm, m, stream);
+        if (kpad == 128 && bias_mode == 0) return launch_variant<128, 0, true>(prm, m, stream);
     }
     switch (kpad) {
         case 32: return launch_kpad<32>(prm, bias_mode, m, stream);
@@ -786,5 +946,5 @@ extern "C" void ba_debug_tcgen05_logits(int32_t* dev_S, int head) {
     ba::tc::g_dbg_S = dev_S;
     ba::tc::g_dbg_head = head;
 }
-// Dev hook: per-CTA clock64 timeline, [ctas][4 roles][128] int64 (zero-filled by the caller).
+// Dev hook: per-CTA clock64 timeline, [ctas][4 roles][256] int64 (zero-filled by the caller).
 extern "C" void ba_debug_tcgen05_timeline(long long* dev_T) { ba::tc::g_dbg_T = dev_T; }
