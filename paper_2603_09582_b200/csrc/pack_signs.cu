@@ -45,6 +45,7 @@ struct Vec16;
 template <>
 struct Vec16<__nv_bfloat16> {
     static constexpr int kElems = 8;
+    static constexpr bool kIsBf16 = true;
     __device__ static void unpack(const uint4& v, float (&f)[8]) {
         const uint32_t r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -55,9 +56,35 @@ struct Vec16<__nv_bfloat16> {
     }
 };
 
+// bf16 fast path: 8 sign bits and sum |x| of one 16-byte vector without per-element compares.
+// A bf16 is negative-and-nonzero (bit = 0) iff its sign bit is set and its magnitude bits are not all zero; for a pair
+// packed in a u32, (mag + 0x7FFF7FFF) sets bit 15 / 31 exactly when that half's magnitude is nonzero (no carry crosses
+// the halves because mag <= 0x7FFF), so neg = w & (mag + 0x7FFF7FFF) & 0x80008000.  -0.0 therefore maps to +1 like the
+// reference's `x >= 0` (bitops.cpp:45).
+__device__ __forceinline__ void bf16x8_signs_abs(const uint4& v, unsigned int& bits, float& sum_abs) {
+    const uint32_t r[4] = {v.x, v.y, v.z, v.w};
+    uint32_t neg[4];
+    float sa = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t mag = r[i] & 0x7FFF7FFFu;
+        neg[i] = r[i] & (mag + 0x7FFF7FFFu) & 0x80008000u;
+        sa += __uint_as_float(mag << 16);          // |even element|
+        sa += __uint_as_float(mag & 0xFFFF0000u);  // |odd element|
+    }
+    // bytes 1 and 3 of every word carry the flags in their top bit: gather the 8 flag bytes, then the 8 bits
+    const uint32_t lo = __byte_perm(neg[0], neg[1], 0x7531);  // elements 0..3 -> bytes 0..3
+    const uint32_t hi = __byte_perm(neg[2], neg[3], 0x7531);  // elements 4..7
+    const uint32_t nlo = ((lo >> 7) * 0x01020408u) >> 24;     // bit k = flag of byte k (flags are the only bits set)
+    const uint32_t nhi = ((hi >> 7) * 0x01020408u) >> 24;
+    bits = ~(nlo | (nhi << 4)) & 0xFFu;
+    sum_abs = sa;
+}
+
 template <>
 struct Vec16<__half> {
     static constexpr int kElems = 8;
+    static constexpr bool kIsBf16 = false;
     __device__ static void unpack(const uint4& v, float (&f)[8]) {
         const uint32_t r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -73,6 +100,7 @@ struct Vec16<__half> {
 template <>
 struct Vec16<float> {
     static constexpr int kElems = 4;
+    static constexpr bool kIsBf16 = false;
     __device__ static void unpack(const uint4& v, float (&f)[4]) {
         f[0] = __uint_as_float(v.x);
         f[1] = __uint_as_float(v.y);
@@ -159,14 +187,18 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_vec_kernel(const __gr
 #pragma unroll
         for (int u = 0; u < kPackUnroll; ++u) {
             if (s0 + u * kPackThreads >= slots) break;  // block-uniform
-            float f[EPV];
-            Vec16<T>::unpack(v[u], f);
             unsigned int m = 0;
             float sa = 0.f;
+            if (sizeof(T) == 2 && Vec16<T>::kIsBf16) {
+                bf16x8_signs_abs(v[u], m, sa);
+            } else {
+                float f[EPV];
+                Vec16<T>::unpack(v[u], f);
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-                m |= (f[e] >= 0.0f ? 1u : 0u) << e;  // -0.0f >= 0 is true, NaN is false: the reference's rule
-                sa += fabsf(f[e]);
+                for (int e = 0; e < EPV; ++e) {
+                    m |= (f[e] >= 0.0f ? 1u : 0u) << e;  // -0.0f >= 0 is true, NaN is false: the reference's rule
+                    sa += fabsf(f[e]);
+                }
             }
             if (!act[u]) m = 0;
             acc += sa;
