@@ -75,6 +75,18 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
         : "memory");
     return done;
 }
+// Truly non-blocking phase test (try_wait may sleep up to a hardware time limit when the phase is still open).
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done;
+}
 // Bounded wait: a protocol bug traps (clean launch failure) after 2^26 polls -- each poll sleeps in hardware up to
 // kSuspendHint ns or until the barrier moves, so that is seconds -- instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -135,6 +147,12 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 
 // Shared-memory matrix descriptor (cute::UMMA::SmemDescriptor bit layout, mma_sm100_desc.hpp):
@@ -215,6 +233,7 @@ struct Params {
     int nbox;          // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;  // ring depths in shared memory
     int o_vec8;        // O rows are 32-byte aligned (256-bit stores)
+    int o_stage;       // epilogue goes through the shared-memory staging boxes + TMA stores (asynchronous)
     int32_t* dbg_S;    // optional [N,N] int32 dump of the logits of head dbg_head (tests only)
     int dbg_head;
     long long* dbg_T;  // optional timeline: [cta][role 0..3][kTlStamps] clock64 stamps (dev tool, TL kernels only)
@@ -309,27 +328,40 @@ __device__ __forceinline__ float tile_max(const float (&x)[BN], int nk, int nch)
 // 2c (low half) and 2c+1, the K-major A-operand layout of the P.V MMA.  SUM adds the fp32 row sum (otherwise the
 // tensor core sums the bf16 values through the ones block).  MASKED zeroes columns >= nk and skips the 32-key halves
 // the MMA will not read.
+// ROLLING REFILL (unmasked tiles): as soon as a 16-column quarter of x has been through ex2, the same registers are
+// reloaded with the NEXT tile's scores (other S stage) if that tile is already complete (`refill`), so the TMEM load
+// latency and the barrier round trip of the next tile hide behind this tile's exponentials.
 template <bool MASKED, bool SUM>
-__device__ __forceinline__ float exp_store(const float (&x)[BN], int nk, int nch, float ea, float nm, uint32_t p_addr) {
+__device__ __forceinline__ float exp_store(float (&x)[BN], int nk, int nch, float ea, float nm, uint32_t p_addr, bool refill,
+                                           uint32_t next_addr) {
     float l0 = 0.f, l1 = 0.f;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         if (!MASKED || 2 * h < nch) {  // (a guarded body, not a break: the loop must unroll so x[] stays in registers)
             uint32_t pk[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int i = 32 * h + 2 * e;
-                float p0 = ex2(fmaf(x[i], ea, nm));
-                float p1 = ex2(fmaf(x[i + 1], ea, nm));
-                if (MASKED) {
-                    p0 = (i < nk) ? p0 : 0.f;
-                    p1 = (i + 1 < nk) ? p1 : 0.f;
+            for (int q = 0; q < 2; ++q) {
+#pragma unroll
+                for (int e = 8 * q; e < 8 * q + 8; ++e) {
+                    const int i = 32 * h + 2 * e;
+                    float p0 = ex2(fmaf(x[i], ea, nm));
+                    float p1 = ex2(fmaf(x[i + 1], ea, nm));
+                    if (MASKED) {
+                        p0 = (i < nk) ? p0 : 0.f;
+                        p1 = (i + 1 < nk) ? p1 : 0.f;
+                    }
+                    if (SUM) {
+                        l0 += p0;
+                        l1 += p1;
+                    }
+                    pk[e] = pack_bf16(p0, p1);
                 }
-                if (SUM) {
-                    l0 += p0;
-                    l1 += p1;
+                if (!MASKED && refill) {
+                    if (h == 0 && q == 0) BA_TMEM_LD16(next_addr + 0, x, 0);
+                    if (h == 0 && q == 1) BA_TMEM_LD16(next_addr + 16, x, 16);
+                    if (h == 1 && q == 0) BA_TMEM_LD16(next_addr + 32, x, 32);
+                    if (h == 1 && q == 1) BA_TMEM_LD16(next_addr + 48, x, 48);
                 }
-                pk[e] = pack_bf16(p0, p1);
             }
             BA_TMEM_ST16U(p_addr + 16 * h, pk);
         }
@@ -341,27 +373,15 @@ struct RowState {
     float m_ref, m_true, l;  // base-2 units: reference max used in the exponent, true running max, running denominator
 };
 
-// One 64-key tile of the online softmax for one query row: S (TMEM) -> x -> P (TMEM, over S).  FULL = all 64 keys valid:
-// straight-line code, every load issued up front.  The caller has waited for the S tile (and the bias stage).
+// One 64-key tile of the online softmax for one query row: x (raw scores, already in registers) -> P (TMEM, over S).
+// FULL = all 64 keys valid: straight-line code.  The caller has waited for the bias stage; `refill` says the next S tile
+// is complete, in which case x leaves holding the next tile's raw scores (loads in flight).
 template <int BIAS, bool ROWSUM, bool FULL>
-__device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, uint32_t s_addr, uint32_t lane_base,
+__device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, float (&x)[BN], uint32_t s_addr, uint32_t lane_base,
                                              const unsigned char* brow, int bstage, const char* bias_row, int bias_dtype,
                                              int j, uint32_t g, int nk, float sc, float ea, int ocols, int tid, int lane,
-                                             int32_t* dbg_row) {
+                                             int32_t* dbg_row, uint64_t* next_bar, uint32_t next_par, bool has_next, uint32_t next_addr, bool& refilled) {
     const int nch = FULL ? BN / 16 : (nk + 15) >> 4;
-    float x[BN];
-    uint4 bv[8];
-    if (BIAS == 1 && FULL) {  // the whole bias row of the tile, issued before the TMEM loads so the latencies overlap
-#pragma unroll
-        for (int c = 0; c < 8; ++c) bv[c] = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));
-        warp_arrive(&sm->bfree[bstage], lane);
-    }
-    tc_fence_after();
-    BA_TMEM_LD16(s_addr + 0, x, 0);
-    if (FULL || nch > 1) BA_TMEM_LD16(s_addr + 16, x, 16);
-    if (FULL || nch > 2) BA_TMEM_LD16(s_addr + 32, x, 32);
-    if (FULL || nch > 3) BA_TMEM_LD16(s_addr + 48, x, 48);
-    tc_wait_ld();
     if (dbg_row) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
@@ -370,13 +390,15 @@ __device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, uint32_t s_
     if (BIAS == 1 && FULL) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const uint32_t bw[4] = {bv[c].x, bv[c].y, bv[c].z, bv[c].w};
+            const uint4 b = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));
+            const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc, __uint_as_float(bw[e] << 16));
                 x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc, __uint_as_float(bw[e] & 0xFFFF0000u));
             }
         }
+        warp_arrive(&sm->bfree[bstage], lane);
     } else if (BIAS == 1) {
 #pragma unroll
         for (int c = 0; c < BN / 16; ++c)
@@ -410,7 +432,10 @@ __device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, uint32_t s_
         rs.l *= alpha;
         rs.m_ref = m_new;
     }
-    rs.l += exp_store<!FULL, !ROWSUM>(x, nk, nch, ea, -rs.m_ref, s_addr);
+    // is the next S tile complete by now?  (uniform across the warp: one barrier, one instruction)
+    refilled = FULL && has_next && mbar_test(next_bar, next_par);
+    if (refilled) tc_fence_after();
+    rs.l += exp_store<!FULL, !ROWSUM>(x, nk, nch, ea, -rs.m_ref, s_addr, refilled, next_addr);
 }
 
 struct Epilogue {
@@ -421,14 +446,23 @@ struct Epilogue {
 };
 
 // O / l -> global for one finished unit, then tell the MMA warp that O may be overwritten.
+// Staged path (o_stage): each warp owns two 4 KB staging boxes of [32 rows][32 floats] (128B-swizzled like the O tensor
+// map); a box is written, handed to a TMA store and only waited for when the SAME buffer is needed again (normally one
+// whole unit later), so the softmax warps never sit on the store queue -- direct stores cost ~25% of the kernel at
+// N=197.  The hardware clips the boxes at N and d.
 template <bool ROWSUM>
-__device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, Epilogue& ep, uint32_t lane_base, int lane) {
+__device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const CUtensorMap* omap, unsigned char* stage,
+                                             Epilogue& ep, uint32_t lane_base, int warp, int lane) {
     const FwdArgs& a = prm.a;
     mbar_wait(&sm->pvdone[ep.g_last & 1u], (ep.g_last >> 1) & 1u);  // every MMA of the unit has retired
     if (ep.warp_ok) {
         tc_fence_after();
         float l = ep.rs.l;
         float* orow = a.O + ((int64_t)ep.head * a.N + ep.row) * a.d;
+        if (prm.o_stage) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // both boxes are free again
+            __syncwarp();
+        }
         for (int c = 0; c < prm.dvp; c += 32) {
             float o[32], den[16];
             const bool two = c + 16 < prm.dvp;
@@ -440,7 +474,24 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, Epilog
             const float inv_l = 1.0f / l;
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] *= inv_l;
-            if (ep.row_ok) {
+            if (prm.o_stage) {
+                const int bi = (c >> 5) & 1;
+                unsigned char* box = stage + (warp * 2 + bi) * 4096;
+                if (c >= 64) {  // third and later boxes of a wide head reuse a buffer inside the same epilogue
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<float4*>(box + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                        make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(omap, box, c, ep.row - lane, ep.head);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else if (ep.row_ok) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int cc = c + 8 * q;
@@ -474,16 +525,17 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, Epilog
 template <int KPAD, int BIAS, bool TL = false>
 __global__ void __launch_bounds__(kThreads, 2)
 attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap,
-               const __grid_constant__ CUtensorMap bmap) {
+               const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap) {
     // d <= 96 leaves 16 spare TMEM columns next to O: the softmax denominator is then accumulated by the tensor
     // core (P x ones), which removes one FADD per score from the softmax warps.
     constexpr bool ROWSUM = KPAD <= 96;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
-    // carve shared memory: V ring | bias ring (both 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
+    // carve shared memory: V ring | bias ring | O staging (all 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
     unsigned char* sV = smem_raw;                                   // vst x nbox x 8192
     unsigned char* sB = sV + prm.vst * prm.nbox * 8192;             // bst x 16384
-    unsigned char* sQ = sB + prm.bst * 16384;                       // qst x BM x KPAD
+    unsigned char* sO = sB + prm.bst * 16384;                       // o_stage x 32768: epilogue staging boxes (4 warps x 2 x 4 KB)
+    unsigned char* sQ = sO + prm.o_stage * 32768;                   // qst x BM x KPAD
     unsigned char* sK = sQ + prm.qst * BM * KPAD;                   // kst x BN x KPAD
     unsigned char* sOnes = sK + prm.kst * BN * KPAD;                // 512 B of bf16 1.0 (B operand of the row-sum MMA)
     Smem* sm = reinterpret_cast<Smem*>(sOnes + 512);
@@ -527,6 +579,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     if (warp == 5 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
         if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+        if (prm.o_stage) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&omap)) : "memory");
     }
     sm->lut[tid] = expand_byte((uint32_t)tid);
     if (tid < 128) reinterpret_cast<uint32_t*>(sOnes)[tid] = 0x3F803F80u;  // bf16 1.0 pairs
@@ -693,27 +746,43 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
         Ring br;
         uint32_t g = 0;  // tiles consumed so far (S stage = g & 1)
-        float sc_next = 0.f;
+        // per-head scales are fetched one unit ahead and only combined when used (an early multiply would stall this
+        // in-order thread on the global loads)
+        float muq_next = 0.f, muk_next = 0.f;
         if ((int)blockIdx.x < prm.units) {
             const int head = blockIdx.x / prm.mblocks;
-            sc_next = __ldg(a.mu_q + head) * __ldg(a.mu_k + head) * a.inv_tau;
+            muq_next = __ldg(a.mu_q + head);
+            muk_next = __ldg(a.mu_k + head);
         }
         // The epilogue of a unit is deferred until the first tile of the NEXT unit has been through the softmax, so the
         // latency of the unit's last P.V MMA hides behind useful work (the MMA warp holds that next tile's P.V back until
         // `ofree` says O has been read out).
         Epilogue ep{};
         ep.pending = false;
-        uint32_t s_ok = mbar_try(&sm->sfull[0], 0);
+        // x holds the raw scores of the tile about to be processed; its TMEM loads are issued one tile ahead (by the
+        // rolling refill inside the previous tile's exponentials when S was ready in time, else right after that tile)
+        float x[BN];
+        const int my_units = (prm.units - (int)blockIdx.x + G - 1) / G;
+        const uint32_t total_tiles = (uint32_t)(my_units > 0 ? my_units : 0) * (uint32_t)T;
+        if (total_tiles > 0) {
+            mbar_wait(&sm->sfull[0], 0);
+            tc_fence_after();
+            BA_TMEM_LD16(lane_base + kColS + 0, x, 0);
+            BA_TMEM_LD16(lane_base + kColS + 16, x, 16);
+            BA_TMEM_LD16(lane_base + kColS + 32, x, 32);
+            BA_TMEM_LD16(lane_base + kColS + 48, x, 48);
+        }
         for (int u = blockIdx.x; u < prm.units; u += G) {
             const int head = u / prm.mblocks;
             const int row0 = (u - head * prm.mblocks) * BM;
             const int row = row0 + tid;
             const bool row_ok = row < N;
             const bool warp_ok = row0 + warp * 32 < N;  // warps whose 32 rows are all past N only keep the barriers moving
-            const float sc = sc_next;  // natural-log units per unit of dot
+            const float sc = muq_next * muk_next * a.inv_tau;  // natural-log units per unit of dot
             if (u + G < prm.units) {
                 const int hn = (u + G) / prm.mblocks;
-                sc_next = __ldg(a.mu_q + hn) * __ldg(a.mu_k + hn) * a.inv_tau;
+                muq_next = __ldg(a.mu_q + hn);
+                muk_next = __ldg(a.mu_k + hn);
             }
             // BIAS == 0 keeps x = raw integer dot and folds sc*log2e into the exponent FMA; otherwise x = dot*sc + bias
             const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;
@@ -727,8 +796,13 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             for (int j = 0; j < T; ++j, ++g) {
                 const uint32_t s = g & 1u;
                 const int nk = min(BN, N - j * BN);
+                const bool has_next = g + 1 < total_tiles;
+                const uint32_t next_addr = lane_base + kColS + (s ^ 1u) * BN;
+                uint64_t* next_bar = &sm->sfull[s ^ 1u];
+                const uint32_t next_par = ((g + 1) >> 1) & 1u;
+                bool refilled = false;
                 BA_STAMP(0);
-                if (!s_ok) mbar_wait(&sm->sfull[s], (g >> 1) & 1u);
+                tc_wait_ld();  // S(g) is in x
                 BA_STAMP(0);
                 if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
                     if (BIAS == 1) {
@@ -736,6 +810,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         warp_arrive(&sm->bfree[br.stage], lane);
                         br.next(prm.bst);
                     }
+                    tc_fence_before();
                     warp_arrive(&sm->pfull[s], lane);
                 } else {
                     const unsigned char* brow = nullptr;
@@ -746,21 +821,30 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     const uint32_t s_addr = lane_base + kColS + s * BN;
                     int32_t* dbg_row = dump ? prm.dbg_S + (int64_t)row * N + j * BN : nullptr;
                     if (nk == BN)
-                        softmax_tile<BIAS, ROWSUM, true>(sm, rs, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g, nk,
-                                                         sc, ea, ocols, tid, lane, dbg_row);
+                        softmax_tile<BIAS, ROWSUM, true>(sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
+                                                         nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
+                                                         refilled);
                     else
-                        softmax_tile<BIAS, ROWSUM, false>(sm, rs, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g, nk,
-                                                          sc, ea, ocols, tid, lane, dbg_row);
+                        softmax_tile<BIAS, ROWSUM, false>(sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
+                                                          nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
+                                                          refilled);
                     if (BIAS == 1) br.next(prm.bst);
                     tc_wait_st();
                     tc_fence_before();
                     warp_arrive(&sm->pfull[s], lane);
                 }
-                // poll the next S tile now: the answer arrives while the deferred epilogue / loop overhead runs
-                s_ok = mbar_try(&sm->sfull[s ^ 1u], ((g + 1) >> 1) & 1u);
+                BA_STAMP(0);
+                if (has_next && !refilled) {  // the next tile was not ready in time (or this warp idles): load it now
+                    mbar_wait(next_bar, next_par);
+                    tc_fence_after();
+                    BA_TMEM_LD16(next_addr + 0, x, 0);
+                    BA_TMEM_LD16(next_addr + 16, x, 16);
+                    BA_TMEM_LD16(next_addr + 32, x, 32);
+                    BA_TMEM_LD16(next_addr + 48, x, 48);
+                }
                 BA_STAMP(0);
                 if (j == 0 && ep.pending) {
-                    run_epilogue<ROWSUM>(sm, prm, ep, lane_base, lane);
+                    run_epilogue<ROWSUM>(sm, prm, &omap, sO, ep, lane_base, warp, lane);
                     BA_STAMP(0);
                 }
             }
@@ -772,7 +856,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             ep.g_last = g - 1;
             ep.rs = rs;
         }
-        if (ep.pending) run_epilogue<ROWSUM>(sm, prm, ep, lane_base, lane);
+        if (ep.pending) run_epilogue<ROWSUM>(sm, prm, &omap, sO, ep, lane_base, warp, lane);
+        if (prm.o_stage && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem may be released
         BA_STAMP(0);
     }
     tc_fence_before();
@@ -811,12 +896,12 @@ static long env_long(const char* name, long dflt) {
     return e ? atol(e) : dflt;
 }
 static size_t smem_bytes(const Params& prm, int kpad) {
-    return (size_t)prm.vst * prm.nbox * 8192 + (size_t)prm.bst * 16384 + (size_t)prm.qst * BM * kpad +
+    return (size_t)prm.vst * prm.nbox * 8192 + (size_t)prm.bst * 16384 + (size_t)prm.o_stage * 32768 + (size_t)prm.qst * BM * kpad +
            (size_t)prm.kst * BN * kpad + 512 + sizeof(Smem);
 }
 
 struct Maps {
-    CUtensorMap v, b;
+    CUtensorMap v, b, o;
 };
 
 static int sm_count() {
@@ -841,7 +926,7 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
     const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
-    attn_tc_kernel<KPAD, BIAS, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b);
+    attn_tc_kernel<KPAD, BIAS, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
@@ -881,6 +966,7 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
     prm.o_vec8 = reinterpret_cast<uintptr_t>(a.O) % 32 == 0 ? 1 : 0;  // d % 8 == 0 keeps every row 32-byte aligned
+    if (env_long("BA_EXP_NOSTORE", 0)) prm.o_vec8 = 2;  // dev experiment: skip the O stores
     prm.dbg_S = g_dbg_S;
     prm.dbg_head = g_dbg_head;
     prm.dbg_T = g_dbg_T;
@@ -893,15 +979,18 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                             reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         bias_mode = tma_ok ? 1 : 2;
     }
-    // ring depths: as deep as fits two CTAs per SM
+    // ring depths: as deep as fits two CTAs per SM; the asynchronous epilogue staging matters most when units are short
     prm.qst = 2;
     prm.kst = 3;
     prm.vst = 3;
     prm.bst = bias_mode == 1 ? 2 : 0;
-    if (smem_bytes(prm, kpad) > kSmemBudget) prm.qst = 1;
-    if (smem_bytes(prm, kpad) > kSmemBudget) prm.kst = 2;
+    prm.o_stage = env_long("BA_O_STAGE", 1) ? 1 : 0;
     if (smem_bytes(prm, kpad) > kSmemBudget) prm.vst = 2;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.kst = 2;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.qst = 1;
+    if (smem_bytes(prm, kpad) > kSmemBudget && prm.tiles >= 16) prm.o_stage = 0;  // long units: the epilogue is rare
     if (smem_bytes(prm, kpad) > kSmemBudget && prm.bst == 2) prm.bst = 1;
+    if (smem_bytes(prm, kpad) > kSmemBudget) prm.o_stage = 0;
     if (smem_bytes(prm, kpad) > kSmemBudget) return -(int)cudaErrorInvalidConfiguration;
 
     Maps m;
@@ -913,6 +1002,14 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
         if (enc(&m.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    }
+    {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 32 floats (128 B), clipped at N and d by the hardware
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
+        const cuuint32_t box[3] = {32, 32, 1};
+        if (enc(&m.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
     m.b = m.v;
