@@ -189,6 +189,29 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^x on the FMA / ALU pipes (Cody-Waite split + degree-3 minimax polynomial, max relative error 7.5e-5 -- far below
+// the bf16 rounding of P): a fixed share of the exponentials of every tile goes here instead of the 16-per-clock MUFU
+// unit, which is the pipe the softmax warps queue on.  x <= ~8 by the lazy-rescale rule; x below -125 is clamped
+// (2^-125 is zero for every purpose here and keeps the exponent arithmetic in range).
+#ifndef BA_POLY_NOBIAS
+#define BA_POLY_NOBIAS 0  // of every 16 exponentials, without a bias tile (measured: any share > 0 is slower)
+#endif
+#ifndef BA_POLY_BIAS
+#define BA_POLY_BIAS 0    // of every 16 exponentials, with a bias tile
+#endif
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;        // 1.5 * 2^23: round(x) lands in the low mantissa bits
+    const float f = x - (t - 12582912.0f);  // [-0.5, 0.5]
+    float p = fmaf(0.0551717501f, f, 0.242611319f);
+    p = fmaf(p, f, 0.693260968f);
+    p = fmaf(p, f, 0.999928057f);
+    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));  // p * 2^round(x)
+}
+template <int POLY>
+__device__ __forceinline__ float ex2_mix(float x, int i) {  // i is a compile-time column index after unrolling
+    return (((i & 15) * POLY) & 15) < POLY ? ex2_poly(x) : ex2(x);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -278,6 +301,11 @@ __device__ __forceinline__ void expand_store(unsigned char* tile, int rows, int 
     }
 }
 
+#define BA_STAMP(role)                                                                         \
+    do {                                                                                       \
+        if (TL && tl_buf && tl_n < kTlStamps) tl_buf[(role) * kTlStamps + tl_n++] = clock64(); \
+    } while (0)
+
 // ------------------------------------------------------------------------------------------------ softmax pieces
 // Scores of one 16-column chunk: x = dot*sc + bias.  BIAS 1 reads the bf16 tile staged by TMA (row `tid` of a
 // 128 x 64 tile, 128B swizzle), BIAS 2 reads the table directly.
@@ -331,7 +359,7 @@ __device__ __forceinline__ float tile_max(const float (&x)[BN], int nk, int nch)
 // ROLLING REFILL (unmasked tiles): as soon as a 16-column quarter of x has been through ex2, the same registers are
 // reloaded with the NEXT tile's scores (other S stage) if that tile is already complete (`refill`), so the TMEM load
 // latency and the barrier round trip of the next tile hide behind this tile's exponentials.
-template <bool MASKED, bool SUM>
+template <bool MASKED, bool SUM, int POLY>
 __device__ __forceinline__ float exp_store(float (&x)[BN], int nk, int nch, float ea, float nm, uint32_t p_addr, bool refill,
                                            uint32_t next_addr) {
     float l0 = 0.f, l1 = 0.f;
@@ -344,8 +372,8 @@ __device__ __forceinline__ float exp_store(float (&x)[BN], int nk, int nch, floa
 #pragma unroll
                 for (int e = 8 * q; e < 8 * q + 8; ++e) {
                     const int i = 32 * h + 2 * e;
-                    float p0 = ex2(fmaf(x[i], ea, nm));
-                    float p1 = ex2(fmaf(x[i + 1], ea, nm));
+                    float p0 = ex2_mix<POLY>(fmaf(x[i], ea, nm), i);
+                    float p1 = ex2_mix<POLY>(fmaf(x[i + 1], ea, nm), i + 1);
                     if (MASKED) {
                         p0 = (i < nk) ? p0 : 0.f;
                         p1 = (i + 1 < nk) ? p1 : 0.f;
@@ -376,8 +404,8 @@ struct RowState {
 // One 64-key tile of the online softmax for one query row: x (raw scores, already in registers) -> P (TMEM, over S).
 // FULL = all 64 keys valid: straight-line code.  The caller has waited for the bias stage; `refill` says the next S tile
 // is complete, in which case x leaves holding the next tile's raw scores (loads in flight).
-template <int BIAS, bool ROWSUM, bool FULL>
-__device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, float (&x)[BN], uint32_t s_addr, uint32_t lane_base,
+template <int BIAS, bool ROWSUM, bool FULL, bool TL>
+__device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem* sm, RowState& rs, float (&x)[BN], uint32_t s_addr, uint32_t lane_base,
                                              const unsigned char* brow, int bstage, const char* bias_row, int bias_dtype,
                                              int j, uint32_t g, int nk, float sc, float ea, int ocols, int tid, int lane,
                                              int32_t* dbg_row, uint64_t* next_bar, uint32_t next_par, bool has_next, uint32_t next_addr, bool& refilled) {
@@ -409,6 +437,7 @@ __device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, float (&x)[
         for (int c = 0; c < BN / 16; ++c)
             if (c < nch) bias_chunk<2>(x, c, sc, nullptr, tid, bias_row, bias_dtype, j * BN, nk);
     }
+    BA_STAMP(0);
     float tmax = tile_max<!FULL>(x, nk, nch);
     tmax *= ea;  // ea >= 0, so the max commutes with the scaling
     rs.m_true = fmaxf(rs.m_true, tmax);
@@ -432,10 +461,12 @@ __device__ __forceinline__ void softmax_tile(Smem* sm, RowState& rs, float (&x)[
         rs.l *= alpha;
         rs.m_ref = m_new;
     }
+    BA_STAMP(0);
     // is the next S tile complete by now?  (uniform across the warp: one barrier, one instruction)
     refilled = FULL && has_next && mbar_test(next_bar, next_par);
     if (refilled) tc_fence_after();
-    rs.l += exp_store<!FULL, !ROWSUM>(x, nk, nch, ea, -rs.m_ref, s_addr, refilled, next_addr);
+    rs.l += exp_store<!FULL, !ROWSUM, (BIAS == 0 ? BA_POLY_NOBIAS : BA_POLY_BIAS)>(x, nk, nch, ea, -rs.m_ref, s_addr, refilled, next_addr);
+    BA_STAMP(0);
 }
 
 struct Epilogue {
@@ -516,10 +547,6 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
     ep.pending = false;
 }
 
-#define BA_STAMP(role)                                                                         \
-    do {                                                                                       \
-        if (TL && tl_buf && tl_n < kTlStamps) tl_buf[(role) * kTlStamps + tl_n++] = clock64(); \
-    } while (0)
 
 // BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
 template <int KPAD, int BIAS, bool TL = false>
@@ -821,15 +848,16 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     const uint32_t s_addr = lane_base + kColS + s * BN;
                     int32_t* dbg_row = dump ? prm.dbg_S + (int64_t)row * N + j * BN : nullptr;
                     if (nk == BN)
-                        softmax_tile<BIAS, ROWSUM, true>(sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
+                        softmax_tile<BIAS, ROWSUM, true, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
                                                          nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
                                                          refilled);
                     else
-                        softmax_tile<BIAS, ROWSUM, false>(sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
+                        softmax_tile<BIAS, ROWSUM, false, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
                                                           nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
                                                           refilled);
                     if (BIAS == 1) br.next(prm.bst);
                     tc_wait_st();
+                    BA_STAMP(0);
                     tc_fence_before();
                     warp_arrive(&sm->pfull[s], lane);
                 }
