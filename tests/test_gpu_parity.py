@@ -97,7 +97,7 @@ def test_binary_logits_bit_exact(ba, port, n, d):
 
 
 # ------------------------------------------------------------------------------------------ K2 fused attention
-def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None):
+def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None, tol=None):
     """heads: list of (q,k,v,bias) float64; bias_mode in {None,'per_head','shared'}."""
     import torch
     H = len(heads)
@@ -120,7 +120,7 @@ def run_and_compare(ba, port, heads, n, d, dtype, bias_mode, scale=None):
             tau = None if scale is None else 1.0 / scale
             y, om, ol = port.binary_attention_fused(q, k, v, tau=tau, bias=b)
             err = np.abs(O[0, h] - y).max()
-            assert err <= TOL_O, f"{kern}: head {h} max-abs {err:.3e}"
+            assert err <= (tol or {}).get(kern, TOL_O), f"{kern}: head {h} max-abs {err:.3e}"
             # log-sum-exp is tile-invariant: m + ln(l)  (AttentionOutput::row_max/row_sum, attention.hpp:45-46)
             # (the tcgen05 kernel's row_sum is the sum of the bf16-rounded weights it actually multiplied with V,
             #  accumulated by the tensor core: each weight is within 2^-9 relative of exp(S-m), so ln(l) is within
@@ -234,6 +234,42 @@ def test_host_buffer_entry_point(ba, port):
     out = ba.forward_host(Qh, Kh, Vh, bh)
     dev = ba.forward(Qh.cuda(), Kh.cuda(), Vh.cuda(), bh.cuda())
     assert torch.equal(out, dev.cpu())
+
+
+def test_host_buffer_pipeline_chunks(ba):
+    """The host entry point cuts the head grid into chunks that flow through copy-in / compute / copy-out streams.
+    360 heads of 25 KB make three chunks whose boundaries (166, 332) are not multiples of H, so the per-head bias
+    lookup of a ranged call (head0 offset) is exercised too; results must equal the one-shot device call bit for bit."""
+    import torch
+    B, H, n, d = 30, 12, 197, 64
+    g = torch.Generator().manual_seed(3)
+    Qh, Kh, Vh = (torch.randn(B, H, n, d, generator=g).to(torch.bfloat16).pin_memory() for _ in range(3))
+    bh = (0.5 * torch.randn(H, n, n, generator=g)).to(torch.bfloat16).pin_memory()
+    for bias in (bh, None):
+        out = ba.forward_host(Qh, Kh, Vh, bias)
+        dev = ba.forward(Qh.cuda(), Kh.cuda(), Vh.cuda(), None if bias is None else bias.cuda())
+        assert torch.equal(out, dev.cpu())
+
+
+@pytest.mark.parametrize("n,d,with_bias", [(1500, 64, True), (2048, 128, False), (1111, 72, True)])
+def test_long_sequence_rows_match_oracle(ba, port, n, d, with_bias):
+    """BASELINE.json configs[3]/[4] regime (many key tiles per unit, the rolling S refill and the lazy rescale at
+    work): two heads against the oracle, every row."""
+    heads = [make_head_inputs(port, 21, s, n, d, bias_scale=0.5 if with_bias else None) for s in range(2)]
+    run_and_compare(ba, port, heads, n, d, "bf16", "per_head" if with_bias else None)
+
+
+def test_large_logit_scale_rescale_path(ba, port):
+    """Inputs scaled by 16 make mu_q*mu_k/tau ~ 20 per unit of dot: row maxima move by far more than the lazy-rescale
+    threshold from tile to tile, so the O/l rescale branch runs for real; the result must still match the oracle.
+    In this regime a row's weight sits on two or three tied keys, so the 2^-9 rounding of each bf16 weight no longer
+    averages out: the tensor-core path is held to 3 * 2^-9 * max|V| (~6e-3 * 1) instead of the typical-input bar."""
+    n, d = 300, 64
+    heads = []
+    for s in range(2):
+        q, k, v, b = make_head_inputs(port, 22, s, n, d, bias_scale=0.5)
+        heads.append((q * 16.0, k * 16.0, v, b))  # power of two: still exactly representable in bf16
+    run_and_compare(ba, port, heads, n, d, "bf16", "per_head", tol={"tcgen05": 6e-3})
 
 
 def test_error_codes_on_device(ba):
