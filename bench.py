@@ -348,7 +348,16 @@ def main():
         achieved = pv_flops / (k2_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_sustained"]}
-    roof.update({"traffic": None, "kernel": f"K2 fused attention ({used})", "kernel_ms": k2_ms,
+    # DRAM traffic of the same kernel from this round's `ncu --set full` capture (profiles/r01_ncu_traffic.json, bytes
+    # per launch; only captured for the default workload with its dense bias)
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        if args.workload == "c2" and bias is not None and used == "tcgen05":
+            traffic = tj["c2"]["k2_attn"]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        traffic = None
+    roof.update({"traffic": traffic, "kernel": f"K2 fused attention ({used})", "kernel_ms": k2_ms,
                  "algorithmic_bytes": k2_bytes, "peak_source": pk["source"],
                  "k1_pack": {"ms": k1_ms, "algorithmic_bytes": k1_bytes,
                              "achieved_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None},
@@ -378,8 +387,11 @@ def main():
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "ba_binary_attention_host (pinned host buffers)"},
             "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "dense_bf16_ms": dense,
-            "speedup_vs_dense_bf16": (min(x for x in (dense.get("nobias"), dense.get("bias")) if x) / ms_per_step)
-            if dense and (dense.get("nobias") or dense.get("bias")) else None}
+            # like for like: dense attention WITH the same additive bias table when this run has one
+            "speedup_vs_dense_bf16": (dense.get("bias" if bias is not None else "nobias") / ms_per_step)
+            if dense and dense.get("bias" if bias is not None else "nobias") else None,
+            "speedup_vs_dense_bf16_without_bias": (dense.get("nobias") / ms_per_step)
+            if dense and dense.get("nobias") else None}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -170,19 +170,33 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_vec_kernel(const __gr
     const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * (int64_t)sizeof(T);
     uint64_t* wbase = job.words + ((int64_t)head * N + row0) * w64;
 
+    // Lane slot s = pass * kPackThreads + tid  ->  (row, vector-in-row).  When the slots per row divide the CTA size
+    // (d = 64, 72, 128, 256 ...: vprp is 8, 16 or 32) the vector index is the same in every pass and the row advances by
+    // a constant, so the loop carries no division; other head dims take the general mapping.  (ncu on the first
+    // version: 137 instructions per 16-byte vector, ALU pipe 75% busy -- index arithmetic, not HBM, was the limit.)
+    const bool regular = (kPackThreads % vprp) == 0;
+    const int vs_fix = threadIdx.x % vprp, row_fix = threadIdx.x / vprp, row_step = kPackThreads / vprp;
+    const bool lane_act = vs_fix < vpr;
     float acc = 0.f;
     for (int s0 = 0; s0 < slots; s0 += kPackThreads * kPackUnroll) {
         uint4 v[kPackUnroll];
         int rowl[kPackUnroll], vs[kPackUnroll];
         bool act[kPackUnroll];
+        const int pass0 = s0 / kPackThreads;
 #pragma unroll
         for (int u = 0; u < kPackUnroll; ++u) {
-            const int s = s0 + u * kPackThreads + threadIdx.x;
-            rowl[u] = s / vprp;
-            vs[u] = s - rowl[u] * vprp;
-            act[u] = (s < slots) && (vs[u] < vpr);
+            if (regular) {
+                rowl[u] = (pass0 + u) * row_step + row_fix;
+                vs[u] = vs_fix;
+                act[u] = lane_act && rowl[u] < rows;
+            } else {
+                const int s = s0 + u * kPackThreads + threadIdx.x;
+                rowl[u] = s / vprp;
+                vs[u] = s - rowl[u] * vprp;
+                act[u] = (s < slots) && (vs[u] < vpr);
+            }
             v[u] = make_uint4(0, 0, 0, 0);
-            if (act[u]) v[u] = ldg_nc_16(xbase + ((int64_t)rowl[u] * vpr + vs[u]) * 16);
+            if (act[u]) v[u] = ldg_nc_16(xbase + (uint32_t)(rowl[u] * vpr + vs[u]) * 16u);
         }
 #pragma unroll
         for (int u = 0; u < kPackUnroll; ++u) {
@@ -206,8 +220,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_vec_kernel(const __gr
 #pragma unroll
             for (int off = 1; off < HALF; off <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, off);
             const unsigned int hi = __shfl_down_sync(0xffffffffu, w, HALF);
-            if (g == 0 && (s0 + u * kPackThreads + threadIdx.x) < slots)
-                wbase[(int64_t)rowl[u] * w64 + vs[u] / LPG] = ((uint64_t)hi << 32) | (uint64_t)w;
+            if (g == 0 && rowl[u] < rows) wbase[(uint32_t)(rowl[u] * w64 + vs[u] / LPG)] = ((uint64_t)hi << 32) | (uint64_t)w;
         }
     }
     finish_head_sum(acc, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
