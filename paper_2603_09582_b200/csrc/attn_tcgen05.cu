@@ -41,6 +41,7 @@ constexpr int kThreads = 256;
 constexpr int kTmemCols = 256;
 constexpr int kColS = 0, kColO = 128;
 constexpr int kMaxStages = 4;
+constexpr int kFoldMax = 8;        // trailing keys that can be folded into the last full tile (CUDA-core logits, 5th P.V k-step)
 constexpr int kRegsSoftmax = 200, kRegsCtrl = 56;  // setmaxnreg split of the 2 x 128 x 128 register pool
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kSuspendHint = 0x989680;  // try_wait may sleep this long before re-polling (cuts spin instructions)
@@ -256,6 +257,8 @@ struct Params {
     int nbox;          // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;  // ring depths in shared memory
     int o_vec8;        // O rows are 32-byte aligned (256-bit stores)
+    int fold;          // 1..8: that many trailing keys (N % 64) ride along with the last full tile instead of a tile of their own
+    int vbox;          // bytes of one 64-column V box in shared memory (64 keys, or 80 with folding)
     int o_stage;       // epilogue goes through the shared-memory staging boxes + TMA stores (asynchronous)
     int32_t* dbg_S;    // optional [N,N] int32 dump of the logits of head dbg_head (tests only)
     int dbg_head;
@@ -408,7 +411,8 @@ template <int BIAS, bool ROWSUM, bool FULL, bool TL>
 __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem* sm, RowState& rs, float (&x)[BN], uint32_t s_addr, uint32_t lane_base,
                                              const unsigned char* brow, int bstage, const char* bias_row, int bias_dtype,
                                              int j, uint32_t g, int nk, float sc, float ea, int ocols, int tid, int lane,
-                                             int32_t* dbg_row, uint64_t* next_bar, uint32_t next_par, bool has_next, uint32_t next_addr, bool& refilled) {
+                                             int32_t* dbg_row, uint64_t* next_bar, uint32_t next_par, bool has_next, uint32_t next_addr, bool& refilled,
+                                             const float (&xt)[kFoldMax], int nt) {
     const int nch = FULL ? BN / 16 : (nk + 15) >> 4;
     if (dbg_row) {
 #pragma unroll
@@ -439,6 +443,10 @@ __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem*
     }
     BA_STAMP(0);
     float tmax = tile_max<!FULL>(x, nk, nch);
+    if (FULL && nt > 0) {  // folded trailing keys (xt already holds dot*sc + bias, -inf past nt)
+#pragma unroll
+        for (int i = 0; i < kFoldMax; ++i) tmax = fmaxf(tmax, xt[i]);
+    }
     tmax *= ea;  // ea >= 0, so the max commutes with the scaling
     rs.m_true = fmaxf(rs.m_true, tmax);
     // lazy rescale (first tile: m_ref = -inf forces it with alpha = 0 on the still-unwritten O)
@@ -466,6 +474,22 @@ __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem*
     refilled = FULL && has_next && mbar_test(next_bar, next_par);
     if (refilled) tc_fence_after();
     rs.l += exp_store<!FULL, !ROWSUM, (BIAS == 0 ? BA_POLY_NOBIAS : BA_POLY_BIAS)>(x, nk, nch, ea, -rs.m_ref, s_addr, refilled, next_addr);
+    if (FULL && nt > 0) {  // weights of the folded keys: P columns 32..39 (keys 64..79 of this tile; -inf -> 0)
+        uint32_t pk[8];
+        float lt = 0.f;
+#pragma unroll
+        for (int e = 0; e < kFoldMax / 2; ++e) {
+            const float p0 = ex2(fmaf(xt[2 * e], ea, -rs.m_ref)), p1 = ex2(fmaf(xt[2 * e + 1], ea, -rs.m_ref));
+            lt += p0 + p1;
+            pk[e] = pack_bf16(p0, p1);
+        }
+#pragma unroll
+        for (int e = kFoldMax / 2; e < 8; ++e) pk[e] = 0u;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0,%1,%2,%3,%4,%5,%6,%7};" ::"r"(pk[0]), "r"(pk[1]), "r"(pk[2]),
+                     "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]), "r"(s_addr + 32)
+                     : "memory");
+        if (!ROWSUM) rs.l += lt;
+    }
     BA_STAMP(0);
 }
 
@@ -549,18 +573,19 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
 
 
 // BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
-template <int KPAD, int BIAS, bool TL = false>
+template <int KPAD, int BIAS, bool FOLD, bool TL = false>
 __global__ void __launch_bounds__(kThreads, 2)
 attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap,
-               const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap) {
+               const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap,
+               const __grid_constant__ CUtensorMap vmap16) {
     // d <= 96 leaves 16 spare TMEM columns next to O: the softmax denominator is then accumulated by the tensor
     // core (P x ones), which removes one FADD per score from the softmax warps.
     constexpr bool ROWSUM = KPAD <= 96;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
     // carve shared memory: V ring | bias ring | O staging (all 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
-    unsigned char* sV = smem_raw;                                   // vst x nbox x 8192
-    unsigned char* sB = sV + prm.vst * prm.nbox * 8192;             // bst x 16384
+    unsigned char* sV = smem_raw;                                   // vst x nbox x vbox (8192, or 10240 with folding)
+    unsigned char* sB = sV + prm.vst * prm.nbox * prm.vbox;         // bst x 16384
     unsigned char* sO = sB + prm.bst * 16384;                       // o_stage x 32768: epilogue staging boxes (4 warps x 2 x 4 KB)
     unsigned char* sQ = sO + prm.o_stage * 32768;                   // qst x BM x KPAD
     unsigned char* sK = sQ + prm.qst * BM * KPAD;                   // kst x BN x KPAD
@@ -630,7 +655,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                                  ((uint32_t)(BM >> 4) << 24);
         const uint64_t q_desc = make_desc(smem_u32(sQ), BM * 16, 128, 0);     // K-major no swizzle; +ks*2*BM*16 per K step
         const uint64_t k_desc = make_desc(smem_u32(sK), BN * 16, 128, 0);     // +s*BN*KPAD per stage, +ks*2*BN*16 per K step
-        const uint64_t v_desc = make_desc(smem_u32(sV), 8192, 1024, 2);       // MN-major 128B swizzle; +ks*2048 per 16 keys
+        const uint64_t v_desc = make_desc(smem_u32(sV), (uint32_t)prm.vbox, 1024, 2);  // MN-major 128B swizzle; +ks*2048 per 16 keys
         const uint64_t ones_desc = make_desc(smem_u32(sOnes), 256, 128, 0);   // 16 x 16 block of ones: any layout reads 1.0
         Ring qr, kr, vr;
         uint32_t g = 0;  // tiles issued so far by this CTA (S stage = g & 1)
@@ -648,10 +673,10 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             tc_fence_after();
             const int ksteps = (pend_nk + 15) >> 4;
             const uint32_t p_tmem = tmem + kColS + s * BN;
-            const uint64_t vd = v_desc + (uint64_t)((vr.stage * prm.nbox * 8192) >> 4);
+            const uint64_t vd = v_desc + (uint64_t)((vr.stage * prm.nbox * prm.vbox) >> 4);
             if (elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < BN / 16; ++ks) {
+                for (int ks = 0; ks < BN / 16 + (FOLD ? 1 : 0); ++ks) {  // (the fifth step only exists for a folded tail)
                     if (ks < ksteps) {
                         const uint32_t acc = (pend_j > 0 || ks > 0) ? 1u : 0u;
                         mma_bf16_ts(tmem + kColO, p_tmem + ks * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv, acc);
@@ -691,7 +716,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 pend_g = g;
                 pend_j = j;
                 pend_unit = unit_i;
-                pend_nk = min(BN, N - j * BN);
+                pend_nk = (FOLD && j == T - 1) ? BN + prm.fold : min(BN, N - j * BN);
                 ++g;
             }
             qr.next(prm.qst);
@@ -715,9 +740,13 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     BA_STAMP(2);
                     mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
                     BA_STAMP(2);
-                    mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * 8192);
-                    for (int b = 0; b < prm.nbox; ++b)
-                        tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * 8192, b * 64, j * BN, head);
+                    const bool folded = FOLD && j == T - 1;  // this tile carries the 1..8 trailing keys as 16 more V rows
+                    mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * (folded ? 8192 + 2048 : 8192));
+                    for (int b = 0; b < prm.nbox; ++b) {
+                        unsigned char* dst = sV + (vr.stage * prm.nbox + b) * prm.vbox;
+                        tma_load_3d(&vmap, &sm->vfull[vr.stage], dst, b * 64, j * BN, head);
+                        if (folded) tma_load_3d(&vmap16, &sm->vfull[vr.stage], dst + 8192, b * 64, (j + 1) * BN, head);
+                    }
                     vr.next(prm.vst);
                 }
             }
@@ -819,6 +848,40 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                            ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
             RowState rs{-INFINITY, -INFINITY, 0.f};
             const bool dump = prm.dbg_S && head == prm.dbg_head && row_ok;
+            // folded tail keys (prm.fold of them): this row's packed query and those keys' packed words / bias values are
+            // requested now and only turned into logits at the unit's last tile, so the loads cost no wait
+            constexpr int W = (KPAD + 63) / 64;
+            constexpr int NF = FOLD ? kFoldMax : 1;
+            uint64_t fq[W], fk[NF][W];
+            float fb[NF];
+            if (FOLD && warp_ok) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) fq[w] = (row_ok && w < w64) ? __ldg(a.q_words + ((int64_t)head * N + row) * w64 + w) : 0ull;
+#pragma unroll
+                for (int i = 0; i < NF; ++i) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+                        fk[i][w] = (i < prm.fold && w < w64) ? __ldg(a.k_words + ((int64_t)head * N + T * BN + i) * w64 + w) : 0ull;
+                    fb[i] = 0.f;
+                }
+                if (BIAS != 0 && row_ok) {
+                    const char* brow_g = static_cast<const char*>(a.bias) +
+                                         ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                    if (BIAS == 1) {  // bf16 rows padded to 16 bytes: the 8 columns after the last full tile are one vector
+                        const uint4 b = __ldg(reinterpret_cast<const uint4*>(brow_g + (size_t)T * BN * 2));
+                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                        for (int e = 0; e < NF / 2; ++e) {
+                            fb[2 * e] = __uint_as_float(bw[e] << 16);
+                            fb[2 * e + 1] = __uint_as_float(bw[e] & 0xFFFF0000u);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NF; ++i)
+                            if (i < prm.fold) fb[i] = load_as_float(brow_g, a.bias_dtype, T * BN + i);
+                    }
+                }
+            }
 
             for (int j = 0; j < T; ++j, ++g) {
                 const uint32_t s = g & 1u;
@@ -847,14 +910,32 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     }
                     const uint32_t s_addr = lane_base + kColS + s * BN;
                     int32_t* dbg_row = dump ? prm.dbg_S + (int64_t)row * N + j * BN : nullptr;
+                    float xt[kFoldMax];
+                    int nt = 0;
+#pragma unroll
+                    for (int i = 0; i < kFoldMax; ++i) xt[i] = -INFINITY;
+                    if (FOLD && j == T - 1) {  // logits of the folded keys: d - 2*popc(q xor k) (bitops.cpp:59-67)
+                        nt = prm.fold;
+#pragma unroll
+                        for (int i = 0; i < NF; ++i) {
+                            int pc = 0;
+#pragma unroll
+                            for (int w = 0; w < W; ++w) pc += __popcll(fq[w] ^ fk[i][w]);
+                            const float dot = (float)(d - 2 * pc);
+                            if (i < nt) {
+                                xt[i] = (BIAS == 0) ? dot : fmaf(dot, sc, fb[i]);
+                                if (dbg_row) dbg_row[BN + i] = d - 2 * pc;
+                            }
+                        }
+                    }
                     if (nk == BN)
                         softmax_tile<BIAS, ROWSUM, true, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
                                                          nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
-                                                         refilled);
+                                                         refilled, xt, nt);
                     else
                         softmax_tile<BIAS, ROWSUM, false, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
                                                           nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
-                                                          refilled);
+                                                          refilled, xt, nt);
                     if (BIAS == 1) br.next(prm.bst);
                     tc_wait_st();
                     BA_STAMP(0);
@@ -924,12 +1005,12 @@ static long env_long(const char* name, long dflt) {
     return e ? atol(e) : dflt;
 }
 static size_t smem_bytes(const Params& prm, int kpad) {
-    return (size_t)prm.vst * prm.nbox * 8192 + (size_t)prm.bst * 16384 + (size_t)prm.o_stage * 32768 + (size_t)prm.qst * BM * kpad +
+    return (size_t)prm.vst * prm.nbox * prm.vbox + (size_t)prm.bst * 16384 + (size_t)prm.o_stage * 32768 + (size_t)prm.qst * BM * kpad +
            (size_t)prm.kst * BN * kpad + 512 + sizeof(Smem);
 }
 
 struct Maps {
-    CUtensorMap v, b, o;
+    CUtensorMap v, b, o, v16;
 };
 
 static int sm_count() {
@@ -943,28 +1024,35 @@ static int sm_count() {
     return n;
 }
 
-template <int KPAD, int BIAS, bool TL>
+template <int KPAD, int BIAS, bool FOLD, bool TL>
 static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, FOLD, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)kSmemBudget);
         if (e != cudaSuccess) return -(int)e;
         configured = true;
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
     const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
-    attn_tc_kernel<KPAD, BIAS, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o);
+    attn_tc_kernel<KPAD, BIAS, FOLD, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o, m.v16);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
 template <int KPAD>
 static int launch_kpad(const Params& prm, int bias_mode, const Maps& m, cudaStream_t stream) {
+    if (prm.fold) {
+        switch (bias_mode) {
+            case 0: return launch_variant<KPAD, 0, true, false>(prm, m, stream);
+            case 1: return launch_variant<KPAD, 1, true, false>(prm, m, stream);
+            default: return launch_variant<KPAD, 2, true, false>(prm, m, stream);
+        }
+    }
     switch (bias_mode) {
-        case 0: return launch_variant<KPAD, 0, false>(prm, m, stream);
-        case 1: return launch_variant<KPAD, 1, false>(prm, m, stream);
-        default: return launch_variant<KPAD, 2, false>(prm, m, stream);
+        case 0: return launch_variant<KPAD, 0, false, false>(prm, m, stream);
+        case 1: return launch_variant<KPAD, 1, false, false>(prm, m, stream);
+        default: return launch_variant<KPAD, 2, false, false>(prm, m, stream);
     }
 }
 
@@ -990,6 +1078,15 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.a = a;
     prm.mblocks = (a.N + BM - 1) / BM;
     prm.tiles = (a.N + BN - 1) / BN;
+    // tail folding: when only 1..8 keys spill past the last full tile (N = 197: 5), they do not get a tile of their own
+    // -- a tile costs the same pipeline round trip whether it holds 5 keys or 64 -- but ride along with the last full
+    // tile: logits by xor/popc on the CUDA cores, weights in P columns 32..39, V rows in a fifth P.V k-step
+    prm.fold = 0;
+    if (a.N > BN && a.N % BN >= 1 && a.N % BN <= kFoldMax && env_long("BA_FOLD", 1)) {
+        prm.fold = a.N % BN;
+        prm.tiles = a.N / BN;
+    }
+    prm.vbox = prm.fold ? 8192 + 2048 : 8192;
     prm.units = a.BH * prm.mblocks;
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
@@ -1032,6 +1129,16 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
+    m.v16 = m.v;
+    if (prm.fold) {  // 16-key boxes for the folded tail rows (zero fill past N)
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 2, (cuuint64_t)a.N * a.d * 2};
+        const cuuint32_t box[3] = {64, 16, 1};
+        if (enc(&m.v16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    }
     {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 32 floats (128 B), clipped at N and d by the hardware
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
         const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
@@ -1051,9 +1158,10 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
             return -(int)cudaErrorInvalidValue;
     }
     if (g_dbg_T) {  // timeline build of three representative variants (dev tool)
-        if (kpad == 64 && bias_mode == 1) return launch_variant<64, 1, true>(prm, m, stream);
-        if (kpad == 64 && bias_mode == 0) return launch_variant<64, 0, true>(prm, m, stream);
-        if (kpad == 128 && bias_mode == 0) return launch_variant<128, 0, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 1 && prm.fold) return launch_variant<64, 1, true, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 1) return launch_variant<64, 1, false, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 0 && !prm.fold) return launch_variant<64, 0, false, true>(prm, m, stream);
+        if (kpad == 128 && bias_mode == 0 && !prm.fold) return launch_variant<128, 0, false, true>(prm, m, stream);
     }
     switch (kpad) {
         case 32: return launch_kpad<32>(prm, bias_mode, m, stream);

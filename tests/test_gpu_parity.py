@@ -259,6 +259,25 @@ def test_long_sequence_rows_match_oracle(ba, port, n, d, with_bias):
     run_and_compare(ba, port, heads, n, d, "bf16", "per_head" if with_bias else None)
 
 
+@pytest.mark.parametrize("n,d", [(65, 64), (72, 64), (73, 64), (200, 64), (201, 64), (133, 128), (136, 72)])
+@pytest.mark.parametrize("bias_kind", [None, "bf16", "f32"])
+def test_tail_folding_edges(ba, port, n, d, bias_kind):
+    """1..8 keys past the last full 64-key tile are folded into that tile (CUDA-core logits + a fifth P.V k-step);
+    9 or more get a tile of their own.  Both sides of the switch, the shortest folded sequence (65), both bias
+    paths (bf16 table staged by TMA / fp32 table read directly), d = 128 (register denominators) and d = 72."""
+    import torch
+    heads = [make_head_inputs(port, 23, s, n, d, bias_scale=0.5 if bias_kind else None) for s in range(2)]
+    if bias_kind != "f32":
+        run_and_compare(ba, port, heads, n, d, "bf16", "per_head" if bias_kind else None)
+        return
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
+    bias = to_torch(np.stack([h[3] for h in heads]), "f32")  # bf16-representable values in an fp32 table
+    O = ba.forward(Q, K, V, bias, kernel="tcgen05").cpu().numpy().astype(np.float64)
+    for h in range(2):
+        q, k, v, b = heads[h]
+        assert np.abs(O[0, h] - port.binary_attention_fused(q, k, v, bias=b)[0]).max() <= TOL_O
+
+
 def test_large_logit_scale_rescale_path(ba, port):
     """Inputs scaled by 16 make mu_q*mu_k/tau ~ 20 per unit of dot: row maxima move by far more than the lazy-rescale
     threshold from tile to tile, so the O/l rescale branch runs for real; the result must still match the oracle.
@@ -310,7 +329,7 @@ def test_full_size_c2_properties(ba, port):
         assert (Op - O[:8]).abs().max().item() <= TOL_O
 
 
-@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 32), (300, 96)])
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 32), (300, 96), (200, 64), (72, 128)])
 def test_tensor_core_logits_bit_exact(ba, port, n, d):
     """The e4m3 +-1 tcgen05 contraction inside the fused kernel reproduces the integer logits exactly
     (debug dump of the TMEM accumulators; BASELINE.json: 'integer QK^T logits must be bit-exact')."""
