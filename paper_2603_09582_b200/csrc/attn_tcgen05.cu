@@ -186,9 +186,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
                  : "memory")
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef BA_EXP_NOMUFU
+    return x * 0.001f;  // dev experiment: wrong numbers, no MUFU
+#else
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#endif
 }
 // 2^x on the FMA / ALU pipes (Cody-Waite split + degree-3 minimax polynomial, max relative error 7.5e-5 -- far below
 // the bf16 rounding of P): a fixed share of the exponentials of every tile goes here instead of the 16-per-clock MUFU
@@ -213,10 +217,23 @@ template <int POLY>
 __device__ __forceinline__ float ex2_mix(float x, int i) {  // i is a compile-time column index after unrolling
     return (((i & 15) * POLY) & 15) < POLY ? ex2_poly(x) : ex2(x);
 }
+// Packed fp32 FMA (Blackwell FFMA2): two independent a*b+c per instruction.  The softmax warps are bound by issue
+// slots and latency, not by FMA throughput, so halving the FFMA count of the score and exponent-argument math pays.
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+#ifdef BA_EXP_NOF2FP
+    // round-half-up on the integer pipe: add half an ulp, keep the top halves (one PRMT)
+    return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
+#else
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+#endif
 }
 __device__ __forceinline__ void stg_256(float* p, const float* v) {
     asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]),
@@ -322,10 +339,9 @@ __device__ __forceinline__ void bias_chunk(float (&x)[BN], int c16, float sc, co
             const uint4 b = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));
             const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc, __uint_as_float(bw[e] << 16));
-                x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc, __uint_as_float(bw[e] & 0xFFFF0000u));
-            }
+            for (int e = 0; e < 4; ++e)
+                fma2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], sc, sc,
+                     __uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xFFFF0000u));
         }
     } else if (BIAS == 2) {
 #pragma unroll
@@ -375,8 +391,10 @@ __device__ __forceinline__ float exp_store(float (&x)[BN], int nk, int nch, floa
 #pragma unroll
                 for (int e = 8 * q; e < 8 * q + 8; ++e) {
                     const int i = 32 * h + 2 * e;
-                    float p0 = ex2_mix<POLY>(fmaf(x[i], ea, nm), i);
-                    float p1 = ex2_mix<POLY>(fmaf(x[i + 1], ea, nm), i + 1);
+                    float a0, a1;
+                    fma2(a0, a1, x[i], x[i + 1], ea, ea, nm, nm);
+                    float p0 = ex2_mix<POLY>(a0, i);
+                    float p1 = ex2_mix<POLY>(a1, i + 1);
                     if (MASKED) {
                         p0 = (i < nk) ? p0 : 0.f;
                         p1 = (i + 1 < nk) ? p1 : 0.f;
@@ -425,10 +443,9 @@ __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem*
             const uint4 b = *reinterpret_cast<const uint4*>(brow + ((c ^ (tid & 7)) << 4));
             const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                x[c * 8 + 2 * e] = fmaf(x[c * 8 + 2 * e], sc, __uint_as_float(bw[e] << 16));
-                x[c * 8 + 2 * e + 1] = fmaf(x[c * 8 + 2 * e + 1], sc, __uint_as_float(bw[e] & 0xFFFF0000u));
-            }
+            for (int e = 0; e < 4; ++e)
+                fma2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], sc, sc,
+                     __uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xFFFF0000u));
         }
         warp_arrive(&sm->bfree[bstage], lane);
     } else if (BIAS == 1) {
