@@ -64,6 +64,8 @@ with open(out_path, "w") as fo:
                 store = torch.empty(H, N, ld, device="cuda", dtype=torch.bfloat16)
                 store.normal_(0, 0.5)
                 bias = store[:, :, :N]
+            for _ in range(2):  # warm-up (first call builds tensor maps / sets attributes)
+                ba.forward(Q, K, V, bias, kernel="tcgen05")
             ba.profile_begin(4)
             for _ in range(4):
                 ba.forward(Q, K, V, bias, kernel="tcgen05")
