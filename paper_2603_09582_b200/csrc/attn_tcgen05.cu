@@ -418,6 +418,20 @@ __device__ __forceinline__ float exp_store(float (&x)[BN], int nk, int nch, floa
     return l0 + l1;
 }
 
+// O (and the denominator block) of one row times alpha, in tensor memory.  Rare (lazy rescale) and kept out of line so
+// its loop does not sit in the middle of the per-tile code.
+__device__ __noinline__ void rescale_o(uint32_t o_addr, int ocols, float alpha) {
+    tc_fence_after();
+    for (int c = 0; c < ocols; c += 16) {
+        float o[16];
+        BA_TMEM_LD16(o_addr + c, o, 0);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] *= alpha;
+        BA_TMEM_ST16(o_addr + c, o, 0);
+    }
+}
+
 struct RowState {
     float m_ref, m_true, l;  // base-2 units: reference max used in the exponent, true running max, running denominator
 };
@@ -425,14 +439,14 @@ struct RowState {
 // One 64-key tile of the online softmax for one query row: x (raw scores, already in registers) -> P (TMEM, over S).
 // FULL = all 64 keys valid: straight-line code.  The caller has waited for the bias stage; `refill` says the next S tile
 // is complete, in which case x leaves holding the next tile's raw scores (loads in flight).
-template <int BIAS, bool ROWSUM, bool FULL, bool TL>
+template <int BIAS, bool ROWSUM, bool FULL, bool DBG, bool TL>
 __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem* sm, RowState& rs, float (&x)[BN], uint32_t s_addr, uint32_t lane_base,
                                              const unsigned char* brow, int bstage, const char* bias_row, int bias_dtype,
                                              int j, uint32_t g, int nk, float sc, float ea, int ocols, int tid, int lane,
                                              int32_t* dbg_row, uint64_t* next_bar, uint32_t next_par, bool has_next, uint32_t next_addr, bool& refilled,
                                              const float (&xt)[kFoldMax], int nt) {
     const int nch = FULL ? BN / 16 : (nk + 15) >> 4;
-    if (dbg_row) {
+    if (DBG && dbg_row) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
             if (i < nk) dbg_row[i] = (int)x[i];
@@ -473,15 +487,7 @@ __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem*
         const float alpha = need ? ex2(rs.m_ref - m_new) : 1.0f;
         if (j > 0) {
             mbar_wait(&sm->pvdone[(g - 1) & 1u], ((g - 1) >> 1) & 1u);  // P.V of the previous tile has landed in O
-            tc_fence_after();
-            for (int c = 0; c < ocols; c += 16) {
-                float o[16];
-                BA_TMEM_LD16(lane_base + kColO + c, o, 0);
-                tc_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) o[i] *= alpha;
-                BA_TMEM_ST16(lane_base + kColO + c, o, 0);
-            }
+            rescale_o(lane_base + kColO, ocols, alpha);
         }
         rs.l *= alpha;
         rs.m_ref = m_new;
@@ -590,7 +596,12 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
 
 
 // BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
-template <int KPAD, int BIAS, bool FOLD, bool TL = false>
+// MODE: 0 = general (the last key tile may be partial), 1 = 1..8 trailing keys folded into the last full tile,
+//       2 = N is a multiple of 64.  Modes 1 and 2 have no partial tile, so the masked code path is not even compiled in:
+//       the hot loop of the persistent kernel is instruction-fetch sensitive (ncu: ~1/4 of the softmax warps' samples
+//       sit on control flow / no_inst stalls), and the masked variant, the logits dump (DBG, tests only) and the rescale
+//       loop used to sit in the middle of it.
+template <int KPAD, int BIAS, int MODE, bool DBG = false, bool TL = false>
 __global__ void __launch_bounds__(kThreads, 2)
 attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUtensorMap vmap,
                const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap,
@@ -598,6 +609,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     // d <= 96 leaves 16 spare TMEM columns next to O: the softmax denominator is then accumulated by the tensor
     // core (P x ones), which removes one FADD per score from the softmax warps.
     constexpr bool ROWSUM = KPAD <= 96;
+    constexpr bool FOLD = MODE == 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
     // carve shared memory: V ring | bias ring | O staging (all 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
@@ -864,7 +876,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 bias_row = static_cast<const char*>(a.bias) +
                            ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
             RowState rs{-INFINITY, -INFINITY, 0.f};
-            const bool dump = prm.dbg_S && head == prm.dbg_head && row_ok;
+            const bool dump = DBG && prm.dbg_S && head == prm.dbg_head && row_ok;
             // folded tail keys (prm.fold of them): this row's packed query and those keys' packed words / bias values are
             // requested now and only turned into logits at the unit's last tile, so the loads cost no wait
             constexpr int W = (KPAD + 63) / 64;
@@ -941,18 +953,18 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                             const float dot = (float)(d - 2 * pc);
                             if (i < nt) {
                                 xt[i] = (BIAS == 0) ? dot : fmaf(dot, sc, fb[i]);
-                                if (dbg_row) dbg_row[BN + i] = d - 2 * pc;
+                                if (DBG && dbg_row) dbg_row[BN + i] = d - 2 * pc;
                             }
                         }
                     }
-                    if (nk == BN)
-                        softmax_tile<BIAS, ROWSUM, true, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
-                                                         nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
-                                                         refilled, xt, nt);
-                    else
-                        softmax_tile<BIAS, ROWSUM, false, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row, a.bias_dtype, j, g,
-                                                          nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par, has_next, next_addr,
-                                                          refilled, xt, nt);
+                    if (MODE != 0 || nk == BN)
+                        softmax_tile<BIAS, ROWSUM, true, DBG, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row,
+                                                                  a.bias_dtype, j, g, nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par,
+                                                                  has_next, next_addr, refilled, xt, nt);
+                    else if (MODE == 0)
+                        softmax_tile<BIAS, ROWSUM, false, DBG, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row,
+                                                                   a.bias_dtype, j, g, nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par,
+                                                                   has_next, next_addr, refilled, xt, nt);
                     if (BIAS == 1) br.next(prm.bst);
                     tc_wait_st();
                     BA_STAMP(0);
@@ -1041,36 +1053,37 @@ static int sm_count() {
     return n;
 }
 
-template <int KPAD, int BIAS, bool FOLD, bool TL>
+template <int KPAD, int BIAS, int MODE, bool DBG, bool TL>
 static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, FOLD, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)kSmemBudget);
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
         if (e != cudaSuccess) return -(int)e;
         configured = true;
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
     const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
-    attn_tc_kernel<KPAD, BIAS, FOLD, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o, m.v16);
+    attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o, m.v16);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
+template <int KPAD, int MODE>
+static int launch_mode(const Params& prm, int bias_mode, const Maps& m, cudaStream_t stream) {
+    if (prm.dbg_S && bias_mode == 0) return launch_variant<KPAD, 0, MODE, true, false>(prm, m, stream);  // logits dump (tests)
+    switch (bias_mode) {
+        case 0: return launch_variant<KPAD, 0, MODE, false, false>(prm, m, stream);
+        case 1: return launch_variant<KPAD, 1, MODE, false, false>(prm, m, stream);
+        default: return launch_variant<KPAD, 2, MODE, false, false>(prm, m, stream);
+    }
+}
+
 template <int KPAD>
 static int launch_kpad(const Params& prm, int bias_mode, const Maps& m, cudaStream_t stream) {
-    if (prm.fold) {
-        switch (bias_mode) {
-            case 0: return launch_variant<KPAD, 0, true, false>(prm, m, stream);
-            case 1: return launch_variant<KPAD, 1, true, false>(prm, m, stream);
-            default: return launch_variant<KPAD, 2, true, false>(prm, m, stream);
-        }
-    }
-    switch (bias_mode) {
-        case 0: return launch_variant<KPAD, 0, false, false>(prm, m, stream);
-        case 1: return launch_variant<KPAD, 1, false, false>(prm, m, stream);
-        default: return launch_variant<KPAD, 2, false, false>(prm, m, stream);
-    }
+    if (prm.fold) return launch_mode<KPAD, 1>(prm, bias_mode, m, stream);
+    if (prm.a.N % BN == 0) return launch_mode<KPAD, 2>(prm, bias_mode, m, stream);
+    return launch_mode<KPAD, 0>(prm, bias_mode, m, stream);
 }
 
 }  // namespace tc
@@ -1175,10 +1188,11 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
             return -(int)cudaErrorInvalidValue;
     }
     if (g_dbg_T) {  // timeline build of three representative variants (dev tool)
-        if (kpad == 64 && bias_mode == 1 && prm.fold) return launch_variant<64, 1, true, true>(prm, m, stream);
-        if (kpad == 64 && bias_mode == 1) return launch_variant<64, 1, false, true>(prm, m, stream);
-        if (kpad == 64 && bias_mode == 0 && !prm.fold) return launch_variant<64, 0, false, true>(prm, m, stream);
-        if (kpad == 128 && bias_mode == 0 && !prm.fold) return launch_variant<128, 0, false, true>(prm, m, stream);
+        const bool exact = a.N % BN == 0;
+        if (kpad == 64 && bias_mode == 1 && prm.fold) return launch_variant<64, 1, 1, false, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 0 && prm.fold) return launch_variant<64, 0, 1, false, true>(prm, m, stream);
+        if (kpad == 64 && bias_mode == 0 && exact) return launch_variant<64, 0, 2, false, true>(prm, m, stream);
+        if (kpad == 128 && bias_mode == 0 && exact) return launch_variant<128, 0, 2, false, true>(prm, m, stream);
     }
     switch (kpad) {
         case 32: return launch_kpad<32>(prm, bias_mode, m, stream);
