@@ -242,18 +242,17 @@ __device__ __forceinline__ uint4 ldg_nc_16_pred(const void* p, bool pred) {
 
 template <int VPRP>
 __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int chunks) {
-    constexpr int LPG = 8, HALF = 4;                     // lanes per u64 word / per 32-bit half (8 bf16 per lane)
-    constexpr int W64 = VPRP / LPG;                      // u64 words per row
+    constexpr int W64 = VPRP / 8;                        // u64 words per row (one lane slot = 8 bf16 = one byte of signs)
     constexpr int ROWS_PER_PASS = kPackThreads / VPRP;   // rows one pass of the CTA covers
     const PackJob& job = jobs.job[blockIdx.z];
     const int head = blockIdx.x, chunk = blockIdx.y;
     const int vpr = d >> 3;                              // real vectors per row (<= VPRP)
     const int row0 = chunk * kPackRowsPerCta;
     const int rows = min(kPackRowsPerCta, N - row0);
-    const int vs = threadIdx.x & (VPRP - 1), rbase = threadIdx.x / VPRP, g = threadIdx.x & (LPG - 1);
+    const int vs = threadIdx.x & (VPRP - 1), rbase = threadIdx.x / VPRP;
     const bool lane_act = vs < vpr;
     const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * 2 + (rbase * vpr + vs) * 16;
-    uint64_t* wbase = job.words + ((int64_t)head * N + row0) * W64 + rbase * W64 + vs / LPG;
+    unsigned char* wbytes = reinterpret_cast<unsigned char*>(job.words + ((int64_t)head * N + row0) * W64) + rbase * VPRP + vs;
     const int row_bytes = ROWS_PER_PASS * vpr * 16;      // byte stride between a lane's vectors of consecutive passes
     constexpr int PASSES = kPackRowsPerCta / ROWS_PER_PASS;  // 8 (VPRP 8) or 16 (VPRP 16)
     float s0 = 0.f, s1 = 0.f;
@@ -277,14 +276,11 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
             }
             const uint32_t lo = __byte_perm(neg[0], neg[1], 0x7531), hi = __byte_perm(neg[2], neg[3], 0x7531);
             const uint32_t nbits = (((lo >> 7) * 0x01020408u) >> 24) | ((((hi >> 7) * 0x01020408u) >> 24) << 4);
-            // predicated-off lanes loaded zeros = +0.0 -> bit 1: clear them (pad bits and rows past N must be zero)
-            const bool act = lane_act && (p0 + u) * ROWS_PER_PASS + rbase < rows;
-            unsigned int w = act ? ((~nbits & 0xFFu) << (8 * (g & (HALF - 1)))) : 0u;
-            w |= __shfl_xor_sync(0xffffffffu, w, 1);
-            w |= __shfl_xor_sync(0xffffffffu, w, 2);
-            const unsigned int hiw = __shfl_down_sync(0xffffffffu, w, HALF);
-            if (g == 0 && (p0 + u) * ROWS_PER_PASS + rbase < rows)
-                wbase[(p0 + u) * ROWS_PER_PASS * W64] = ((uint64_t)hiw << 32) | (uint64_t)w;
+            // every lane slot owns one BYTE of the packed row (bits 8*vs .. 8*vs+7 of the little-endian u64 words): a warp
+            // writes 32 consecutive bytes with one store, no shuffles.  Idle slots (pad) and predicated-off lanes, whose
+            // zero vector would read as +0.0 -> bit 1, write zero: pad bits must be zero (tensor.hpp:57-94)
+            const bool in_rows = (p0 + u) * ROWS_PER_PASS + rbase < rows;
+            if (in_rows) wbytes[(p0 + u) * ROWS_PER_PASS * VPRP] = lane_act ? (unsigned char)(~nbits & 0xFFu) : (unsigned char)0;
         }
     }
     finish_head_sum(s0 + s1, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
