@@ -75,7 +75,8 @@ struct AttentionConfigT {
     std::size_t block_rows = 64;  // validated like the reference; the CUDA kernels choose their own tiles
     std::size_t block_cols = 64;
     bool quantize_pv = false;
-    std::optional<DenseMatrixT> bias;  // dense N x N table
+    std::optional<DenseMatrixT> bias;  // DenseBias: N x N table (attention.hpp:15-17)
+    std::vector<double> rel1d_offsets;  // Relative1dBias: 2N-1 offsets, b_ij = offsets[i-j+N-1] (attention.hpp:18-21); empty = unused
     Precision precision = Precision::f32;
 
     static AttentionConfigT make(std::size_t n, std::size_t d) {  // attention.cpp:45-53
@@ -128,6 +129,10 @@ public:
             throw ValidationError("attention: block sizes must be in [1, N]");
         if (cfg.bias && (cfg.bias->rows() != n || cfg.bias->cols() != n))
             throw ShapeError("bias: dense table must be N x N");  // attention.cpp:60-61
+        const bool rel1d = !cfg.rel1d_offsets.empty();
+        if (rel1d && cfg.bias) throw ValidationError("bias: give a dense table or relative-1d offsets, not both");
+        if (rel1d && cfg.rel1d_offsets.size() != 2 * n - 1)
+            throw ShapeError("bias: relative-1d offsets must have length 2N-1");  // attention.cpp:66-67
         if (cfg.quantize_pv)
             throw UnsupportedError("quantize_pv=true (int8 P.V) is not built: the CUDA path implements quantize_pv=false");
         if (n == 0 || d == 0) throw ShapeError("binary_quantize: empty matrix");  // quantize.cpp:17
@@ -138,7 +143,7 @@ public:
         p.N = static_cast<int32_t>(n);
         p.d = static_cast<int32_t>(d);
         p.in_dtype = cfg.precision == Precision::bf16 ? BA_BF16 : BA_F32;
-        p.bias_mode = cfg.bias ? BA_BIAS_DENSE : BA_BIAS_NONE;
+        p.bias_mode = cfg.bias ? BA_BIAS_DENSE : rel1d ? BA_BIAS_REL1D : BA_BIAS_NONE;
         p.bias_heads = 1;
         p.bias_dtype = BA_F32;
         p.bias_ld = 0;
@@ -147,6 +152,7 @@ public:
 
         std::vector<float> o(n * d), m(n), l(n), bias32;
         if (cfg.bias) bias32.assign(cfg.bias->data().data(), cfg.bias->data().data() + n * n);
+        if (rel1d) bias32.assign(cfg.rel1d_offsets.begin(), cfg.rel1d_offsets.end());  // the kernels expand it, no N x N table
         if (cfg.precision == Precision::bf16) {
             std::vector<std::uint16_t> hq(n * d), hk(n * d), hv(n * d);
             for (std::size_t i = 0; i < n * d; ++i) {
@@ -154,12 +160,12 @@ public:
                 hk[i] = to_bf16_bits(k.data().data()[i]);
                 hv[i] = to_bf16_bits(v.data().data()[i]);
             }
-            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), cfg.bias ? bias32.data() : nullptr,
+            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), bias32.empty() ? nullptr : bias32.data(),
                                            o.data(), m.data(), l.data()));
         } else {
             std::vector<float> hq(q.data().data(), q.data().data() + n * d), hk(k.data().data(), k.data().data() + n * d),
                 hv(v.data().data(), v.data().data() + n * d);
-            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), cfg.bias ? bias32.data() : nullptr,
+            check(ba_binary_attention_host(h_, &p, hq.data(), hk.data(), hv.data(), bias32.empty() ? nullptr : bias32.data(),
                                            o.data(), m.data(), l.data()));
         }
         return AttentionOutputT<DenseMatrixT>{DenseMatrixT(n, d, std::vector<double>(o.begin(), o.end())),

@@ -47,11 +47,17 @@ typedef enum {
     BA_KERNEL_TCGEN05 = 2  /* +-1 e4m3 QK^T and bf16 P.V on tcgen05/TMEM, V by TMA (bf16, d % 8 == 0, d <= 128) */
 } ba_kernel;
 
-typedef enum { BA_BIAS_NONE = 0, BA_BIAS_DENSE = 1 } ba_bias_mode;
+typedef enum {
+    BA_BIAS_NONE = 0,
+    BA_BIAS_DENSE = 1,  /* DenseBias: N x N table (attention.hpp:15-17, attention.cpp:59-63) */
+    BA_BIAS_REL1D = 2   /* Relative1dBias: b_ij = offsets[i - j + N - 1], 2N-1 entries per table (attention.hpp:18-21,
+                           attention.cpp:65-76); generated inside the kernel, no N x N table ever exists */
+} ba_bias_mode;
 
 /* Q, K, V: [B, H, N, d] row-major contiguous, dtype in_dtype.  O: [B, H, N, d] float32.
  * bias (bias_mode == BA_BIAS_DENSE): [bias_heads, N, bias_ld] with bias_heads in {1, H}; head (b,h)
- * reads table h % bias_heads; bias_ld >= N is the row stride in elements (0 means N). */
+ * reads table h % bias_heads; bias_ld >= N is the row stride in elements (0 means N).
+ * bias (bias_mode == BA_BIAS_REL1D): [bias_heads, 2N-1] contiguous offsets (bias_ld is ignored). */
 typedef struct {
     int32_t B, H, N, d;
     int32_t in_dtype;    /* ba_dtype of Q, K, V */

@@ -96,6 +96,14 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 @dataclass
+class Relative1dBias:
+    """binattn::Relative1dBias (attention.hpp:18-21): b_ij = offsets[i - j + N - 1].  offsets: [2N-1] or [1|H, 2N-1],
+    fp32 or bf16.  Pass it as `bias`: the kernels generate the bias from the table, no N x N tensor is ever built
+    (attention.cpp:65-76 materialises one)."""
+    offsets: torch.Tensor
+
+
+@dataclass
 class AttentionConfig:
     """binattn::AttentionConfig (attention.hpp:29-41).  block_rows/block_cols are accepted and validated like the
     reference's (attention.cpp:26-28) but do not change the result: the CUDA kernels pick their own tiles and the
@@ -106,7 +114,7 @@ class AttentionConfig:
     block_rows: int = 64
     block_cols: int = 64
     quantize_pv: bool = False
-    bias: Optional[torch.Tensor] = None  # dense [N,N] (or [Hb,N,N]) table == materialize_bias output
+    bias: Optional[object] = None  # dense [N,N] (or [Hb,N,N]) table == materialize_bias output, or a Relative1dBias
 
     @staticmethod
     def make(n: int, d: int) -> "AttentionConfig":  # attention.cpp:45-53
@@ -151,12 +159,38 @@ class BinaryAttention:
             raise ValidationError(f"unsupported input dtype {dtype}")
         p = _Params(B=B, H=H, N=N, d=d, in_dtype=_DTYPES[dtype], kernel=KERNELS[kernel])
         p.inv_tau = (1.0 / math.sqrt(d)) if scale is None else float(scale)
-        if bias is not None:
+        if isinstance(bias, Relative1dBias):
+            off = bias.offsets
+            if off.dtype not in (torch.bfloat16, torch.float32):
+                raise ValidationError("bias must be bfloat16 or float32")
+            p.bias_mode, p.bias_heads, p.bias_dtype, p.bias_ld = 2, off.shape[0], _DTYPES[off.dtype], 0
+        elif bias is not None:
             if bias.dtype not in (torch.bfloat16, torch.float32):
                 raise ValidationError("bias must be bfloat16 or float32")
             p.bias_mode, p.bias_heads, p.bias_dtype = 1, bias.shape[0], _DTYPES[bias.dtype]
             p.bias_ld = bias.stride(1)
         return p
+
+    @staticmethod
+    def _check_bias(bias, H, N):
+        """Shape rules of materialize_bias (attention.cpp:59-67); returns the tensor whose pointer goes to the C ABI."""
+        if bias is None:
+            return None, None
+        if isinstance(bias, Relative1dBias):
+            off = bias.offsets
+            if off.dim() == 1:
+                off = off.unsqueeze(0)
+            if off.dim() != 2 or off.shape[1] != 2 * N - 1 or off.shape[0] not in (1, H):
+                raise ShapeError("bias: relative-1d offsets must have length 2N-1")  # attention.cpp:66-67
+            off = off.contiguous()
+            return Relative1dBias(off), off
+        if bias.dim() == 2:
+            bias = bias.unsqueeze(0)
+        if bias.dim() != 3 or bias.shape[1] != N or bias.shape[2] != N or bias.shape[0] not in (1, H):
+            raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
+        if bias.stride(2) != 1 or bias.stride(0) != bias.stride(1) * N:
+            bias = bias.contiguous()
+        return bias, bias
 
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -215,18 +249,12 @@ class BinaryAttention:
             raise ValidationError("Q, K, V must share one dtype")
         B, H, N, d = Q.shape
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
-        if bias is not None:
-            if bias.dim() == 2:
-                bias = bias.unsqueeze(0)
-            if bias.dim() != 3 or bias.shape[1] != N or bias.shape[2] != N or bias.shape[0] not in (1, H):
-                raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
-            if bias.stride(2) != 1 or bias.stride(0) != bias.stride(1) * N:
-                bias = bias.contiguous()
+        bias, bias_t = self._check_bias(bias, H, N)
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
         O = torch.empty((B, H, N, d), dtype=torch.float32, device=Q.device)
         m = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
         l = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
-        _check(self.lib.ba_binary_attention_fwd(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias), _ptr(O),
+        _check(self.lib.ba_binary_attention_fwd(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias_t), _ptr(O),
                                                 _ptr(m), _ptr(l), None, self._stream()))
         return (O, m, l) if return_stats else O
 
@@ -238,14 +266,13 @@ class BinaryAttention:
             raise ShapeError("attention: Q, K, V must be [B,H,N,d]")
         B, H, N, d = Q.shape
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
-        if bias is not None:
-            bias = (bias.unsqueeze(0) if bias.dim() == 2 else bias).contiguous()
-            if bias.shape[1] != N or bias.shape[2] != N or bias.shape[0] not in (1, H):
-                raise ShapeError("bias: dense table must be N x N")
+        bias, bias_t = self._check_bias(bias, H, N)
+        if bias_t is not None and not isinstance(bias, Relative1dBias):
+            bias = bias_t = bias_t.contiguous()
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
         if out is None:
             out = torch.empty((B, H, N, d), dtype=torch.float32, pin_memory=True)
-        _check(self.lib.ba_binary_attention_host(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias), _ptr(out),
+        _check(self.lib.ba_binary_attention_host(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias_t), _ptr(out),
                                                  None, None))
         return out
 
@@ -264,7 +291,7 @@ def binary_attention(Q, K, V, bias=None, scale=None, kernel="auto"):
     """BASELINE.json's operator: binary_attention(Q, K, V, bias, scale) -> O.
 
     Q, K, V: [B,H,N,d] CUDA tensors (bf16 for the tcgen05 kernel; fp16/fp32 run the CUDA-core kernel);
-    bias: None or dense [N,N] / [1|H,N,N] (bf16 or fp32), added before the softmax; scale = 1/temperature
+    bias: None, dense [N,N] / [1|H,N,N] (bf16 or fp32) or Relative1dBias(offsets [1|H, 2N-1]), added before the softmax; scale = 1/temperature
     (default 1/sqrt(d)).  The per-head factor mu_q*mu_k is computed inside, as in the reference."""
     if not Q.is_cuda:
         raise CudaError("binary_attention needs CUDA tensors: this package has no CPU fallback")
@@ -285,7 +312,10 @@ def binary_attention_fused(q, k, v, cfg: AttentionConfig, with_probs: bool = Fal
         raise UnsupportedError("quantize_pv=true (int8 P.V) is not built; the CUDA path implements quantize_pv=false")
     if with_probs:
         raise UnsupportedError("with_probs is diagnostics-only in the reference and is not carried over")
-    if cfg.bias is not None and (cfg.bias.dim() != 2 or cfg.bias.shape[0] != n or cfg.bias.shape[1] != n):
+    if isinstance(cfg.bias, Relative1dBias):
+        if cfg.bias.offsets.dim() != 1 or cfg.bias.offsets.shape[0] != 2 * n - 1:
+            raise ShapeError("bias: relative-1d offsets must have length 2N-1")  # attention.cpp:66-67
+    elif cfg.bias is not None and (cfg.bias.dim() != 2 or cfg.bias.shape[0] != n or cfg.bias.shape[1] != n):
         raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
     ba = _handle_for(q.device)
     O, m, l = ba.forward(q[None, None], k[None, None], v[None, None], cfg.bias, 1.0 / cfg.temperature,

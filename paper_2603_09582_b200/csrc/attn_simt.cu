@@ -39,10 +39,15 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
 
     // scale in the base-2 domain: x2 = dot * (mu_q*mu_k/tau*log2e) + bias*log2e
     const float sc2 = a.mu_q[head] * a.mu_k[head] * a.inv_tau * kLog2e;
+    // dense: pointer to this row of the N x N table, element j; relative-1d (attention.cpp:65-76): pointer to the head's
+    // 2N-1 offsets, element row - j + N - 1
     const char* bias_row = nullptr;
-    if (a.bias && row_ok)
+    const bool rel1d = a.bias_kind == BA_BIAS_REL1D;
+    if (a.bias && row_ok) {
+        const int64_t table = (a.head0 + head) % a.H % a.bias_heads;
         bias_row = static_cast<const char*>(a.bias) +
-                   ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                   (rel1d ? table * (2 * (int64_t)N - 1) : (table * N + row) * a.bias_ld) * dtype_size(a.bias_dtype);
+    }
 
     float o[kSimtSlice];
 #pragma unroll
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
             for (int w = 0; w < kSimtMaxW64; ++w)
                 if (w < w64) diff += __popcll(qb[w] ^ sk[jj * w64 + w]);
             float x2 = (float)(d - 2 * diff) * sc2;
-            if (bias_row) x2 = fmaf(load_as_float(bias_row, a.bias_dtype, j0 + jj), kLog2e, x2);
+            if (bias_row) x2 = fmaf(load_as_float(bias_row, a.bias_dtype, rel1d ? row - (j0 + jj) + N - 1 : j0 + jj), kLog2e, x2);
             if (x2 > m) {  // running-max update (attention.cpp:308-324); first key: alpha = exp2(-inf) = 0
                 const float alpha = exp2f(m - x2);
                 l *= alpha;

@@ -41,6 +41,8 @@ constexpr int kThreads = 256;
 constexpr int kTmemCols = 256;
 constexpr int kColS = 0, kColO = 128;
 constexpr int kMaxStages = 4;
+constexpr int kRelWin = 200;        // floats of the relative-1d bias window of one tile: 8 (folded keys) + 128 + 64 - 1, padded
+constexpr int kRelStage = 1024;    // bytes of one window stage
 constexpr int kFoldMax = 8;        // trailing keys that can be folded into the last full tile (CUDA-core logits, 5th P.V k-step)
 constexpr int kRegsSoftmax = 200, kRegsCtrl = 56;  // setmaxnreg split of the 2 x 128 x 128 register pool
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -273,6 +275,7 @@ struct Params {
     int dvp;           // d rounded up to 16 (UMMA N of P.V)
     int nbox;          // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;  // ring depths in shared memory
+    int bstride;       // bytes of one bias stage: 16384 (dense tile by TMA) or kRelStage (relative-1d window)
     int o_vec8;        // O rows are 32-byte aligned (256-bit stores)
     int fold;          // 1..8: that many trailing keys (N % 64) ride along with the last full tile instead of a tile of their own
     int vbox;          // bytes of one 64-column V box in shared memory (64 keys, or 80 with folding)
@@ -471,6 +474,15 @@ __device__ __forceinline__ void softmax_tile(long long* tl_buf, int& tl_n, Smem*
 #pragma unroll
         for (int c = 0; c < BN / 16; ++c)
             if (c < nch) bias_chunk<2>(x, c, sc, nullptr, tid, bias_row, bias_dtype, j * BN, nk);
+    } else if (BIAS == 3) {
+        // relative-1d bias (attention.cpp:65-76): b(row, col) = offsets[row - col + N - 1]; the producer warp staged the
+        // 191 entries this tile can touch, win[8 + r + 63 - c] for row r and column c of the tile (lanes read
+        // consecutive words: no bank conflicts)
+        const float* win = reinterpret_cast<const float*>(brow) + 8 + tid + 63;
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+            if (FULL || i < nk) x[i] = fmaf(x[i], sc, win[-i]);
+        warp_arrive(&sm->bfree[bstage], lane);
     }
     BA_STAMP(0);
     float tmax = tile_max<!FULL>(x, nk, nch);
@@ -595,7 +607,8 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
 }
 
 
-// BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows)
+// BIAS: 0 = none, 1 = bf16 tile staged by TMA (128B swizzle), 2 = direct global loads (fp32 / unaligned rows),
+//       3 = relative-1d offsets (b_ij = offsets[i-j+N-1]) generated from a per-tile window in shared memory
 // MODE: 0 = general (the last key tile may be partial), 1 = 1..8 trailing keys folded into the last full tile,
 //       2 = N is a multiple of 64.  Modes 1 and 2 have no partial tile, so the masked code path is not even compiled in:
 //       the hot loop of the persistent kernel is instruction-fetch sensitive (ncu: ~1/4 of the softmax warps' samples
@@ -615,7 +628,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     // carve shared memory: V ring | bias ring | O staging (all 1024-aligned for the 128B swizzle) | Q ring | K ring | ones | barriers + table
     unsigned char* sV = smem_raw;                                   // vst x nbox x vbox (8192, or 10240 with folding)
     unsigned char* sB = sV + prm.vst * prm.nbox * prm.vbox;         // bst x 16384
-    unsigned char* sO = sB + prm.bst * 16384;                       // o_stage x 32768: epilogue staging boxes (4 warps x 2 x 4 KB)
+    unsigned char* sO = sB + prm.bst * prm.bstride;                       // o_stage x 32768: epilogue staging boxes (4 warps x 2 x 4 KB)
     unsigned char* sQ = sO + prm.o_stage * 32768;                   // qst x BM x KPAD
     unsigned char* sK = sQ + prm.qst * BM * KPAD;                   // kst x BN x KPAD
     unsigned char* sOnes = sK + prm.kst * BN * KPAD;                // 512 B of bf16 1.0 (B operand of the row-sum MMA)
@@ -645,7 +658,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             mbar_init(&sm->kfree[s], 1);     // tcgen05.commit after the S MMA that read the stage
             mbar_init(&sm->vfull[s], 1);     // expect_tx arrive + TMA bytes
             mbar_init(&sm->vfree[s], 1);     // tcgen05.commit after the P.V MMA that read the stage
-            mbar_init(&sm->bfull[s], 1);     // expect_tx arrive + TMA bytes
+            mbar_init(&sm->bfull[s], BIAS == 3 ? 2 : 1);  // expect_tx arrive + TMA bytes, or one arrival per expander warp (window)
             mbar_init(&sm->bfree[s], 4);     // one elected arrival per softmax warp (bias stage read out)
         }
         mbar_init(&sm->ofree, 4);            // one elected arrival per softmax warp (O read out by the epilogue)
@@ -752,7 +765,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         }
         if (pend) issue_pv();
     } else if (warp == 5) {
-        // ============================================================ TMA producer (V tiles, bias tiles)
+        // ============================================================ TMA producer (V tiles, bias tiles / windows)
         if (lane == 0) {
             Ring vr, br;
             for (int u = blockIdx.x; u < prm.units; u += G) {
@@ -766,24 +779,26 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         tma_load_3d(&bmap, &sm->bfull[br.stage], sB + br.stage * 16384, j * BN, row0, bh);
                         br.next(prm.bst);
                     }
-                    BA_STAMP(2);
-                    mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
-                    BA_STAMP(2);
-                    const bool folded = FOLD && j == T - 1;  // this tile carries the 1..8 trailing keys as 16 more V rows
-                    mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * (folded ? 8192 + 2048 : 8192));
-                    for (int b = 0; b < prm.nbox; ++b) {
-                        unsigned char* dst = sV + (vr.stage * prm.nbox + b) * prm.vbox;
-                        tma_load_3d(&vmap, &sm->vfull[vr.stage], dst, b * 64, j * BN, head);
-                        if (folded) tma_load_3d(&vmap16, &sm->vfull[vr.stage], dst + 8192, b * 64, (j + 1) * BN, head);
+                    if (lane == 0) {
+                        BA_STAMP(2);
+                        mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
+                        BA_STAMP(2);
+                        const bool folded = FOLD && j == T - 1;  // this tile carries the 1..8 trailing keys as 16 more V rows
+                        mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * (folded ? 8192 + 2048 : 8192));
+                        for (int b = 0; b < prm.nbox; ++b) {
+                            unsigned char* dst = sV + (vr.stage * prm.nbox + b) * prm.vbox;
+                            tma_load_3d(&vmap, &sm->vfull[vr.stage], dst, b * 64, j * BN, head);
+                            if (folded) tma_load_3d(&vmap16, &sm->vfull[vr.stage], dst + 8192, b * 64, (j + 1) * BN, head);
+                        }
+                        vr.next(prm.vst);
                     }
-                    vr.next(prm.vst);
                 }
             }
         }
     } else if (warp >= 6) {
         // ============================================================ Q / K expanders
         const int t = tid - 6 * 32;  // 0..63: key t of every K tile, query rows t and t + 64 of every Q tile
-        Ring qr, kr;
+        Ring qr, kr, wr;
         uint32_t wq0[KPAD / 32], wq1[KPAD / 32], wk[KPAD / 32];
         if ((int)blockIdx.x < prm.units) {  // words of the first unit
             const int head = blockIdx.x / prm.mblocks;
@@ -812,6 +827,32 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             }
             for (int j = 0; j < T; ++j) {
                 const int key = j * BN + t;
+                if (BIAS == 3) {
+                    // relative-1d bias: stage the window of the head's 2N-1 offsets this tile can touch (zero outside the
+                    // table); win[0] is entry row0 - 64j - 63 + N - 1 - 8.  The expanders run two to three tiles ahead of
+                    // the softmax, so the L2 round trip of these loads is hidden; all loads are issued before any store.
+                    mbar_wait(&sm->bfree[wr.stage], wr.phase ^ 1u);
+                    float* win = reinterpret_cast<float*>(sB + wr.stage * kRelStage);
+                    const int bh = (a.head0 + head) % a.H % a.bias_heads;
+                    const char* off = static_cast<const char*>(a.bias) + (int64_t)bh * (2 * (int64_t)N - 1) * dtype_size(a.bias_dtype);
+                    const int base = row0 - j * BN - 63 + N - 1 - 8;
+                    constexpr int PER = (kRelWin + 63) / 64;
+                    float wv[PER];
+#pragma unroll
+                    for (int q = 0; q < PER; ++q) {
+                        const int idx = base + t + 64 * q;
+                        wv[q] = 0.f;
+                        if (t + 64 * q < kRelWin && idx >= 0 && idx <= 2 * N - 2) {
+                            if (a.bias_dtype == BA_F32) wv[q] = __ldg(reinterpret_cast<const float*>(off) + idx);
+                            else wv[q] = __uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(off) + idx) << 16);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < PER; ++q)
+                        if (t + 64 * q < kRelWin) win[t + 64 * q] = wv[q];
+                    warp_arrive(&sm->bfull[wr.stage], lane);
+                    wr.next(prm.bst);
+                }
                 mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
                 BA_STAMP(3);
                 expand_store<KPAD>(sK + kr.stage * BN * KPAD, BN, t, wk, d, key < N, sm->lut);
@@ -893,7 +934,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         fk[i][w] = (i < prm.fold && w < w64) ? __ldg(a.k_words + ((int64_t)head * N + T * BN + i) * w64 + w) : 0ull;
                     fb[i] = 0.f;
                 }
-                if (BIAS != 0 && row_ok) {
+                if ((BIAS == 1 || BIAS == 2) && row_ok) {
                     const char* brow_g = static_cast<const char*>(a.bias) +
                                          ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
                     if (BIAS == 1) {  // bf16 rows padded to 16 bytes: the 8 columns after the last full tile are one vector
@@ -924,7 +965,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                 tc_wait_ld();  // S(g) is in x
                 BA_STAMP(0);
                 if (!warp_ok) {  // stay in lock-step with the pipelines, do no math
-                    if (BIAS == 1) {
+                    if (BIAS == 1 || BIAS == 3) {
                         mbar_wait(&sm->bfull[br.stage], br.phase);
                         warp_arrive(&sm->bfree[br.stage], lane);
                         br.next(prm.bst);
@@ -936,6 +977,9 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     if (BIAS == 1) {
                         mbar_wait(&sm->bfull[br.stage], br.phase);
                         brow = sB + br.stage * 16384 + tid * 128;  // row tid of the 128 x 64 bf16 tile
+                    } else if (BIAS == 3) {
+                        mbar_wait(&sm->bfull[br.stage], br.phase);
+                        brow = sB + br.stage * kRelStage;         // the tile's window of relative-1d offsets
                     }
                     const uint32_t s_addr = lane_base + kColS + s * BN;
                     int32_t* dbg_row = dump ? prm.dbg_S + (int64_t)row * N + j * BN : nullptr;
@@ -952,7 +996,9 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                             for (int w = 0; w < W; ++w) pc += __popcll(fq[w] ^ fk[i][w]);
                             const float dot = (float)(d - 2 * pc);
                             if (i < nt) {
-                                xt[i] = (BIAS == 0) ? dot : fmaf(dot, sc, fb[i]);
+                                // relative-1d: column 64 + i of this tile is window entry 8 + r + 63 - (64 + i)
+                                const float bvv = (BIAS == 3) ? reinterpret_cast<const float*>(brow)[8 + tid - 1 - i] : fb[i];
+                                xt[i] = (BIAS == 0) ? dot : fmaf(dot, sc, bvv);
                                 if (DBG && dbg_row) dbg_row[BN + i] = d - 2 * pc;
                             }
                         }
@@ -965,7 +1011,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         softmax_tile<BIAS, ROWSUM, false, DBG, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row,
                                                                    a.bias_dtype, j, g, nk, sc, ea, ocols, tid, lane, dbg_row, next_bar, next_par,
                                                                    has_next, next_addr, refilled, xt, nt);
-                    if (BIAS == 1) br.next(prm.bst);
+                    if (BIAS == 1 || BIAS == 3) br.next(prm.bst);
                     tc_wait_st();
                     BA_STAMP(0);
                     tc_fence_before();
@@ -1034,7 +1080,7 @@ static long env_long(const char* name, long dflt) {
     return e ? atol(e) : dflt;
 }
 static size_t smem_bytes(const Params& prm, int kpad) {
-    return (size_t)prm.vst * prm.nbox * prm.vbox + (size_t)prm.bst * 16384 + (size_t)prm.o_stage * 32768 + (size_t)prm.qst * BM * kpad +
+    return (size_t)prm.vst * prm.nbox * prm.vbox + (size_t)prm.bst * prm.bstride + (size_t)prm.o_stage * 32768 + (size_t)prm.qst * BM * kpad +
            (size_t)prm.kst * BN * kpad + 512 + sizeof(Smem);
 }
 
@@ -1042,25 +1088,31 @@ struct Maps {
     CUtensorMap v, b, o, v16;
 };
 
-static int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+constexpr int kMaxDevices = 64;
+static int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < kMaxDevices) ? dev : 0;
+}
+static int sm_count() {  // per device: one process may hold handles on several GPUs
+    static int n[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!n[dev]) {
+        cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+        if (n[dev] <= 0) n[dev] = 148;
     }
-    return n;
+    return n[dev];
 }
 
 template <int KPAD, int BIAS, int MODE, bool DBG, bool TL>
 static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[kMaxDevices] = {};  // the attribute is per device
+    const int dev = current_device();
+    if (!configured[dev]) {
         const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
         if (e != cudaSuccess) return -(int)e;
-        configured = true;
+        configured[dev] = true;
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
     const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
@@ -1075,6 +1127,7 @@ static int launch_mode(const Params& prm, int bias_mode, const Maps& m, cudaStre
     switch (bias_mode) {
         case 0: return launch_variant<KPAD, 0, MODE, false, false>(prm, m, stream);
         case 1: return launch_variant<KPAD, 1, MODE, false, false>(prm, m, stream);
+        case 3: return launch_variant<KPAD, 3, MODE, false, false>(prm, m, stream);
         default: return launch_variant<KPAD, 2, MODE, false, false>(prm, m, stream);
     }
 }
@@ -1129,7 +1182,9 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
 
     // bias path: a bf16 table with 16-byte aligned rows is staged tile by tile with TMA; anything else is read directly
     int bias_mode = 0;
-    if (a.bias) {
+    if (a.bias && a.bias_kind == BA_BIAS_REL1D) {
+        bias_mode = 3;  // relative-1d offsets: a 191-entry window per tile is staged by the producer warp
+    } else if (a.bias) {
         const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 &&
                             reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         bias_mode = tma_ok ? 1 : 2;
@@ -1138,7 +1193,8 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.qst = 2;
     prm.kst = 3;
     prm.vst = 3;
-    prm.bst = bias_mode == 1 ? 2 : 0;
+    prm.bst = bias_mode == 1 ? 2 : bias_mode == 3 ? 4 : 0;
+    prm.bstride = bias_mode == 3 ? kRelStage : 16384;
     prm.o_stage = env_long("BA_O_STAGE", 1) ? 1 : 0;
     if (smem_bytes(prm, kpad) > kSmemBudget) prm.vst = 2;
     if (smem_bytes(prm, kpad) > kSmemBudget) prm.kst = 2;

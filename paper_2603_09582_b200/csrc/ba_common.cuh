@@ -20,7 +20,8 @@ struct FwdArgs {
     const uint64_t* k_words;  // [BH, N, W64]
     const float* mu_q;        // [BH]
     const float* mu_k;        // [BH]
-    const void* bias;         // [bias_heads, N, bias_ld] or nullptr
+    const void* bias;         // dense: [bias_heads, N, bias_ld]; rel1d: [bias_heads, 2N-1]; or nullptr
+    int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D
     float* O;                 // [BH, N, d] fp32
     float* row_max;           // [BH, N] or nullptr
     float* row_sum;           // [BH, N] or nullptr

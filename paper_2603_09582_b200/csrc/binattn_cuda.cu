@@ -68,8 +68,14 @@ int check_params(const ba_params* p, bool need_attention) {
     if (!need_attention) return BA_OK;
     if (!(p->inv_tau > 0.0f) || !(p->inv_tau < INFINITY))  // attention.cpp:24-25
         return fail(BA_ERR_VALIDATION, "attention: temperature must be positive");
-    if (p->bias_mode != BA_BIAS_NONE && p->bias_mode != BA_BIAS_DENSE)
-        return fail(BA_ERR_VALIDATION, "bias_mode must be BA_BIAS_NONE or BA_BIAS_DENSE");
+    if (p->bias_mode != BA_BIAS_NONE && p->bias_mode != BA_BIAS_DENSE && p->bias_mode != BA_BIAS_REL1D)
+        return fail(BA_ERR_VALIDATION, "bias_mode must be BA_BIAS_NONE, BA_BIAS_DENSE or BA_BIAS_REL1D");
+    if (p->bias_mode == BA_BIAS_REL1D) {
+        if (p->bias_heads != 1 && p->bias_heads != p->H)  // attention.cpp:66-67 (offsets must match the head)
+            return fail(BA_ERR_SHAPE, "bias: relative-1d offsets must be [1 or H, 2N-1]");
+        if (p->bias_dtype != BA_BF16 && p->bias_dtype != BA_F32)
+            return fail(BA_ERR_VALIDATION, "bias_dtype must be BA_BF16 or BA_F32");
+    }
     if (p->bias_mode == BA_BIAS_DENSE) {
         if (p->bias_heads != 1 && p->bias_heads != p->H)  // attention.cpp:60-61 (table must match the head)
             return fail(BA_ERR_SHAPE, "bias: dense table must be [1 or H, N, N]");
@@ -293,7 +299,8 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.k_words = reinterpret_cast<uint64_t*>(ws + L.k_words);
     a.mu_q = reinterpret_cast<float*>(ws + L.mu_q);
     a.mu_k = reinterpret_cast<float*>(ws + L.mu_k);
-    a.bias = p->bias_mode == BA_BIAS_DENSE ? bias : nullptr;
+    a.bias = p->bias_mode != BA_BIAS_NONE ? bias : nullptr;
+    a.bias_kind = p->bias_mode;
     a.O = O;
     a.row_max = row_max;
     a.row_sum = row_sum;
@@ -303,7 +310,7 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.N = p->N;
     a.d = p->d;
     a.W64 = L.W64;
-    a.bias_heads = p->bias_mode == BA_BIAS_DENSE ? p->bias_heads : 1;
+    a.bias_heads = p->bias_mode != BA_BIAS_NONE ? p->bias_heads : 1;
     a.head0 = (int)(head0 % p->H);
     a.bias_dtype = p->bias_dtype;
     a.in_dtype = p->in_dtype;
@@ -346,6 +353,8 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     if (rc) return rc;
     if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
     if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
+    if (p->bias_mode == BA_BIAS_REL1D && !bias)
+        return fail(BA_ERR_SHAPE, "bias: relative-1d offsets must have length 2N-1 (got NULL)");
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     BA_CUDA(cudaSetDevice(h->device));
     int kernel = 0;
@@ -369,7 +378,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     int rc = check_params(p, true);
     if (rc) return rc;
     if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
-    if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
+    if (p->bias_mode != BA_BIAS_NONE && !bias) return fail(BA_ERR_SHAPE, "bias: table / offsets pointer is NULL");
     BA_CUDA(cudaSetDevice(h->device));
     int kernel = 0;
     if ((rc = resolve_kernel(p, &kernel))) return rc;
@@ -379,7 +388,9 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     const size_t head_row = (size_t)p->N * sizeof(float);
     const size_t ld = p->bias_ld ? p->bias_ld : p->N;
     const size_t bias_bytes =
-        p->bias_mode == BA_BIAS_DENSE ? (size_t)p->bias_heads * p->N * ld * ba::dtype_size(p->bias_dtype) : 0;
+        p->bias_mode == BA_BIAS_DENSE   ? (size_t)p->bias_heads * p->N * ld * ba::dtype_size(p->bias_dtype)
+        : p->bias_mode == BA_BIAS_REL1D ? (size_t)p->bias_heads * (2 * (size_t)p->N - 1) * ba::dtype_size(p->bias_dtype)
+                                        : 0;
     // chunking: about 4 MB of each input per chunk, at most kHostChunksMax chunks
     size_t per = (4u << 20) / head_in;
     if (per < 1) per = 1;

@@ -56,22 +56,30 @@ with open(out_path, "w") as fo:
     for (tag, B, H, N, d) in shapes:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
         ld = (N + 7) // 8 * 8
-        for use_bias in (False, True):
+        for use_bias in (False, True, "rel1d"):
             if use_bias and H * N * ld * 2 > (12 << 30):
                 continue
             bias = None
-            if use_bias:
+            ours_bias = None
+            if use_bias is True:
                 store = torch.empty(H, N, ld, device="cuda", dtype=torch.bfloat16)
                 store.normal_(0, 0.5)
-                bias = store[:, :, :N]
+                bias = ours_bias = store[:, :, :N]
+            elif use_bias == "rel1d":
+                # Relative1dBias: ours gets the 2N-1 offsets per head, the dense kernel the N x N table they expand to
+                offs = (0.5 * torch.randn(H, 2 * N - 1, device="cuda")).to(torch.bfloat16).float()
+                idx = torch.arange(N, device="cuda")[:, None] - torch.arange(N, device="cuda")[None, :] + (N - 1)
+                bias = offs[:, idx].to(torch.bfloat16)
+                del idx
+                ours_bias = pkg.Relative1dBias(offs)
             for _ in range(2):  # warm-up (first call builds tensor maps / sets attributes)
-                ba.forward(Q, K, V, bias, kernel="tcgen05")
+                ba.forward(Q, K, V, ours_bias, kernel="tcgen05")
             ba.profile_begin(4)
             for _ in range(4):
-                ba.forward(Q, K, V, bias, kernel="tcgen05")
+                ba.forward(Q, K, V, ours_bias, kernel="tcgen05")
             torch.cuda.synchronize()
             n, k1, k2 = ba.profile_end()
-            ours = time_ms(lambda: ba.forward(Q, K, V, bias, kernel="tcgen05"))
+            ours = time_ms(lambda: ba.forward(Q, K, V, ours_bias, kernel="tcgen05"))
             dense = {}
             dbias = bias.unsqueeze(0).expand(B, H, N, N) if use_bias else None
             for name, fn in dense_candidates(Q, K, V, dbias).items():
@@ -82,7 +90,9 @@ with open(out_path, "w") as fo:
             ok = {k: v for k, v in dense.items() if v}
             best = min(ok, key=ok.get) if ok else None
             ops = 4.0 * B * H * N * N * d
-            rec = {"config": tag, "B": B, "H": H, "N": N, "d": d, "bias": use_bias, "ours_ms": ours,
+            rec = {"config": tag, "B": B, "H": H, "N": N, "d": d,
+                   "bias": {False: "none", True: "dense", "rel1d": "rel1d (ours: 2N-1 offsets; dense: the N x N table)"}[use_bias],
+                   "ours_ms": ours,
                    "k1_pack_ms": k1 / n, "k2_attn_ms": k2 / n, "ours_eff_tops": ops / ours / 1e9,
                    "dense_bf16_ms": dense, "dense_best": best, "dense_best_ms": ok.get(best),
                    "dense_best_eff_tops": ops / ok[best] / 1e9 if best else None,
@@ -90,6 +100,6 @@ with open(out_path, "w") as fo:
                    "timing": "median of 20 (ours) / 10 (dense), CUDA events, L2 flushed between iterations"}
             print(json.dumps(rec), flush=True)
             fo.write(json.dumps(rec) + "\n")
-            del bias
+            del bias, ours_bias
         del Q, K, V
         torch.cuda.empty_cache()

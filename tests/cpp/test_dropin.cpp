@@ -134,6 +134,31 @@ int main() {
             for (std::size_t i = 0; i < c.n * c.d; ++i) CHECK(o2.data().data()[i] == out.output.data().data()[i]);
         }
     }
+    {  // Relative1dBias (attention.hpp:18-21, attention.cpp:65-76): offsets handed to the kernels, table built for the oracle
+        for (Precision prec : {Precision::f32, Precision::bf16}) {
+            const std::size_t n = 197, d = 64;
+            bo_rng_init(rng.data(), 51, 0);
+            const Mat q = rounded(random_dense(rng.data(), n, d), prec), k = rounded(random_dense(rng.data(), n, d), prec),
+                      v = rounded(random_dense(rng.data(), n, d), prec);
+            const Mat off = rounded(random_dense(rng.data(), 1, 2 * n - 1, 0.5), Precision::f32);
+            Cfg cfg = Cfg::make(n, d);
+            cfg.precision = prec;
+            cfg.rel1d_offsets.assign(off.data().data(), off.data().data() + 2 * n - 1);
+            const auto out = eng.binary_attention_fused(q, k, v, cfg);
+            std::vector<double> table(n * n), y(n * d), m(n), l(n);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) table[i * n + j] = cfg.rel1d_offsets[i + n - 1 - j];
+            CHECK(bo_binary_attention_fused(q.data().data(), k.data().data(), v.data().data(), n, d, cfg.temperature,
+                                            cfg.block_rows, cfg.block_cols, 0, table.data(), y.data(), m.data(), l.data()) == 0);
+            double worst = 0.0;
+            for (std::size_t i = 0; i < n * d; ++i) worst = std::fmax(worst, std::fabs(out.output.data().data()[i] - y[i]));
+            std::printf("relative-1d bias N=%zu d=%zu %s  max_abs=%.3e\n", n, d, prec == Precision::bf16 ? "bf16" : "f32", worst);
+            CHECK(worst <= 2e-3);
+            Cfg bad = cfg;
+            bad.rel1d_offsets.pop_back();
+            CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(q, k, v, bad); }));  // attention.cpp:66-67
+        }
+    }
     std::printf(failures ? "FAILED (%d)\n" : "ALL OK\n", failures);
     return failures ? 1 : 0;
 }

@@ -278,6 +278,35 @@ def test_tail_folding_edges(ba, port, n, d, bias_kind):
         assert np.abs(O[0, h] - port.binary_attention_fused(q, k, v, bias=b)[0]).max() <= TOL_O
 
 
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (130, 128), (64, 64), (300, 72), (1000, 64), (40, 200)])
+@pytest.mark.parametrize("per_head", [False, True])
+def test_relative_1d_bias_generated_in_kernel(ba, port, n, d, per_head):
+    """Relative1dBias (attention.hpp:18-21): the kernels build b_ij = offsets[i-j+N-1] from the 2N-1 offsets; the oracle
+    gets the dense table the reference's materialize_bias makes of the same offsets (attention.cpp:65-76).  Also equal,
+    bit for bit, to our own dense-bias path fed that table (same kernel arithmetic, different bias source)."""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    H = 2
+    heads = [make_head_inputs(port, 31, s, n, d) for s in range(H)]
+    rng = np.random.default_rng(7)
+    offs = cpu.bf16_round(0.5 * rng.standard_normal((H if per_head else 1, 2 * n - 1)))
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
+    for odt in ("f32", "bf16"):
+        rel = pkg.Relative1dBias(to_torch(offs, odt))
+        tables = np.stack([port.bias_rel1d(offs[h if per_head else 0], n) for h in range(H)])
+        for kern in kernels_for(ba, 1, H, n, d, "bf16"):
+            O = ba.forward(Q, K, V, rel, kernel=kern)
+            for h in range(H):
+                q, k, v, _ = heads[h]
+                y = port.binary_attention_fused(q, k, v, bias=tables[h])[0]
+                assert np.abs(O[0, h].cpu().numpy().astype(np.float64) - y).max() <= TOL_O, (kern, odt, h)
+            if kern == "tcgen05":
+                dense = ba.forward(Q, K, V, to_torch(tables, "f32"), kernel=kern)
+                assert torch.equal(O, dense)
+    with pytest.raises(pkg.ShapeError):  # attention.cpp:66-67
+        ba.forward(Q, K, V, pkg.Relative1dBias(torch.zeros(2 * n, device="cuda")))
+
+
 def test_large_logit_scale_rescale_path(ba, port):
     """Inputs scaled by 16 make mu_q*mu_k/tau ~ 20 per unit of dot: row maxima move by far more than the lazy-rescale
     threshold from tile to tile, so the O/l rescale branch runs for real; the result must still match the oracle.
