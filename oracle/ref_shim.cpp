@@ -5,6 +5,8 @@
 // /root/reference/proj/src (see oracle/Makefile) into oracle/_ref/libbinattn_ref.so.
 // Nothing from the reference is copied into this repository.  The flat C
 // signatures mirror binattn_oracle.c one-to-one so tests can diff the two.
+#include <functional>
+#include <cstring>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -12,6 +14,8 @@
 #include <vector>
 
 #include "binattn/attention.hpp"
+#include "binattn/errors.hpp"
+#include "binattn/tensor_file.hpp"
 #include "binattn/bitops.hpp"
 #include "binattn/parallel.hpp"
 #include "binattn/quantize.hpp"
@@ -200,6 +204,62 @@ int ref_binary_attention_fused_heads(const double* q, const double* k, const dou
     for (int rc : rcs)
         if (rc) return rc;
     return 0;
+}
+
+// ---- BATF tensor files (tensor_file.hpp:11-23): the reference's own writer / reader, for byte-level interchange checks.
+// Return 0 on success, 2 = FormatError, 3 = IoError, 1 = any other binattn::Error.
+static int guard_file(const std::function<void()>& f) {
+    try {
+        f();
+        return 0;
+    } catch (const FormatError&) {
+        return 2;
+    } catch (const IoError&) {
+        return 3;
+    } catch (const Error&) {
+        return 1;
+    }
+}
+int ref_write_dense(const char* path, const double* data, std::size_t rows, std::size_t cols, int as_f32) {
+    return guard_file([&] {
+        write_tensor(path, DenseMatrix(rows, cols, std::vector<double>(data, data + rows * cols), as_f32 ? Dtype::f32 : Dtype::f64));
+    });
+}
+int ref_write_bits(const char* path, const std::uint64_t* words, std::size_t rows, std::size_t cols) {
+    return guard_file([&] {
+        write_tensor(path, BitMatrix(rows, cols, std::vector<std::uint64_t>(words, words + rows * BitMatrix::words_needed(cols))));
+    });
+}
+// Reads any BATF file with the reference reader; reports dtype code and dims, and copies the payload into the buffer that
+// matches the dtype (dense -> f64 values, packed-bit -> u64 words, int8/uint8 -> bytes, int8 scales -> f64).
+int ref_read_tensor(const char* path, int* dtype, std::size_t* rows, std::size_t* cols, double* dense, std::uint64_t* words,
+                    unsigned char* bytes, double* scales) {
+    return guard_file([&] {
+        const TensorVariant t = read_tensor(path);
+        if (const auto* m = std::get_if<DenseMatrix>(&t)) {
+            *dtype = m->storage() == Dtype::f32 ? 0 : 1;
+            *rows = m->rows();
+            *cols = m->cols();
+            if (dense) std::copy(m->data().begin(), m->data().end(), dense);
+        } else if (const auto* b = std::get_if<BitMatrix>(&t)) {
+            *dtype = 4;
+            *rows = b->rows();
+            *cols = b->logical_cols();
+            if (words) std::copy(b->words().begin(), b->words().end(), words);
+        } else if (const auto* q = std::get_if<QuantizedValues>(&t)) {
+            *dtype = 2;
+            *rows = q->rows();
+            *cols = q->cols();
+            if (bytes) std::memcpy(bytes, q->data().data(), q->data().size());
+            if (scales) std::copy(q->channel_scales().begin(), q->channel_scales().end(), scales);
+        } else {
+            const auto& c = std::get<QuantizedCoeffs>(t);
+            *dtype = 3;
+            *rows = c.rows();
+            *cols = c.cols();
+            if (bytes) std::memcpy(bytes, c.data().data(), c.data().size());
+        }
+    });
 }
 
 } // extern "C"

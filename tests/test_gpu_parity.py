@@ -307,6 +307,50 @@ def test_relative_1d_bias_generated_in_kernel(ba, port, n, d, per_head):
         ba.forward(Q, K, V, pkg.Relative1dBias(torch.zeros(2 * n, device="cuda")))
 
 
+def test_torch_library_op(ba, port):
+    """torch.ops.binattn.binary_attention / _rel1d: same bytes as the handle API, and traceable through the fake kernel."""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    import paper_2603_09582_b200.torch_op  # noqa: F401  (registers the ops)
+    n, d = 197, 64
+    heads = [make_head_inputs(port, 42, s, n, d, bias_scale=0.5) for s in range(2)]
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
+    bias = to_torch(np.stack([h[3] for h in heads]), "bf16")
+    assert torch.equal(torch.ops.binattn.binary_attention(Q, K, V, bias, None), ba.forward(Q, K, V, bias))
+    assert torch.equal(torch.ops.binattn.binary_attention(Q, K, V, None, 0.2), ba.forward(Q, K, V, None, 0.2))
+    off = 0.5 * torch.randn(2, 2 * n - 1, device="cuda")
+    assert torch.equal(torch.ops.binattn.binary_attention_rel1d(Q, K, V, off, None),
+                       ba.forward(Q, K, V, pkg.Relative1dBias(off)))
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    with FakeTensorMode():
+        fq = torch.empty(1, 2, n, d, dtype=torch.bfloat16, device="cuda")
+        out = torch.ops.binattn.binary_attention(fq, fq, fq, None, None)
+        assert out.shape == (1, 2, n, d) and out.dtype == torch.float32
+
+
+def test_packed_planes_as_batf_files(ba, port, tmp_path):
+    """the sign planes K1 writes go to a BATF packed-bit file (dtype 4) byte-identical to the one the
+    oracle's pack produces, and the reference's strict reader (zero pad bits!) accepts it when oracle/_ref is on the box."""
+    import ctypes as C
+    from paper_2603_09582_b200 import batf
+    n, d = 197, 72
+    q = make_head_inputs(port, 41, 0, n, d)[0]
+    words, _ = ba.pack_signs(to_torch(q[None, None], "bf16"))
+    ours, want = tmp_path / "gpu.batf", tmp_path / "cpu.batf"
+    batf.write_tensor(ours, words_to_numpy(words[0, 0]), batf.PACKED_BIT, cols=d)
+    batf.write_tensor(want, port.pack_signs(q), batf.PACKED_BIT, cols=d)
+    assert ours.read_bytes() == want.read_bytes()
+    R = cpu.ref()
+    if R is not None:
+        R.lib.ref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        dt, rows, cols = C.c_int(), C.c_size_t(), C.c_size_t()
+        back = np.zeros((n, 2), np.uint64)
+        assert R.lib.ref_read_tensor(str(ours).encode(), C.byref(dt), C.byref(rows), C.byref(cols), None, back.ctypes.data,
+                                     None, None) == 0
+        assert (dt.value, rows.value, cols.value) == (4, n, d) and np.array_equal(back, port.pack_signs(q))
+
+
 def test_large_logit_scale_rescale_path(ba, port):
     """Inputs scaled by 16 make mu_q*mu_k/tau ~ 20 per unit of dot: row maxima move by far more than the lazy-rescale
     threshold from tile to tile, so the O/l rescale branch runs for real; the result must still match the oracle.
