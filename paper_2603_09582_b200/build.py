@@ -9,7 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbinattn_cuda.so")
-SOURCES = ["binattn_cuda.cu", "pack_signs.cu", "binary_logits.cu", "attn_simt.cu", "attn_tcgen05.cu"]
+SOURCES = ["binattn_cuda.cu", "pack_signs.cu", "binary_logits.cu", "attn_simt.cu", "attn_tcgen05.cu",
+           "attn_tcgen05_k32.cu", "attn_tcgen05_k64.cu", "attn_tcgen05_k96.cu", "attn_tcgen05_k128.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
@@ -29,18 +30,22 @@ def build_extension(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    objs = []
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
-    log = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(PKG, "build", src.replace(".cu", ".o"))
         cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        objs.append(obj)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+    objs, log = [], []
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:  # the translation units are independent
+        for src, obj, r in pool.map(compile_one, SOURCES):
+            log.append(r.stderr)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {src}")
+            objs.append(obj)
     r = subprocess.run([nvcc, "-shared", "-o", LIB, *objs], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
