@@ -133,8 +133,6 @@ public:
         if (rel1d && cfg.bias) throw ValidationError("bias: give a dense table or relative-1d offsets, not both");
         if (rel1d && cfg.rel1d_offsets.size() != 2 * n - 1)
             throw ShapeError("bias: relative-1d offsets must have length 2N-1");  // attention.cpp:66-67
-        if (cfg.quantize_pv)
-            throw UnsupportedError("quantize_pv=true (int8 P.V) is not built: the CUDA path implements quantize_pv=false");
         if (n == 0 || d == 0) throw ShapeError("binary_quantize: empty matrix");  // quantize.cpp:17
 
         ba_params p{};
@@ -149,6 +147,8 @@ public:
         p.bias_ld = 0;
         p.inv_tau = static_cast<float>(1.0 / cfg.temperature);
         p.kernel = BA_KERNEL_AUTO;
+        p.quantize_pv = cfg.quantize_pv ? 1 : 0;  // the reference's default integer P.V mode (CUDA-core kernel)
+        p.block_cols = static_cast<int32_t>(cfg.block_cols);
 
         std::vector<float> o(n * d), m(n), l(n), bias32;
         if (cfg.bias) bias32.assign(cfg.bias->data().data(), cfg.bias->data().data() + n * n);

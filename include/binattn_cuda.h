@@ -67,6 +67,11 @@ typedef struct {
     int64_t bias_ld;     /* elements; 0 -> N */
     float inv_tau;       /* 1 / temperature; must be > 0 (attention.cpp:24-25); use 1/sqrt(d) for AttentionConfig::make */
     int32_t kernel;      /* ba_kernel */
+    int32_t quantize_pv; /* AttentionConfig::quantize_pv (attention.hpp:35): 0 = fp P.V (tensor-core product path),
+                            1 = the reference's default u8 x s8 integer P.V (CUDA-core path) */
+    int32_t block_cols;  /* key-block size of the quantize_pv=1 path (AttentionConfig::block_cols, attention.cpp:50-51):
+                            the u8 weight grid is relative to the running max after each block, so the result depends
+                            on it exactly as the reference's does.  0 -> min(64, N); at most 64.  Ignored otherwise. */
 } ba_params;
 
 typedef struct ba_handle ba_handle;
@@ -85,13 +90,18 @@ size_t ba_workspace_bytes(const ba_params* p);
  *   mu[b,h]         mean |X[b,h,:,:]| (float32; nullable) */
 int ba_pack_signs(ba_handle* h, const ba_params* p, const void* X, uint64_t* words, float* mu, void* stream);
 
+/* quantize_values (quantize.cpp:57-74) for every head of V [B,H,N,d]: vq[b,h,i,c] = round_half_away(V / scales[b,h,c]),
+ * scales[b,h,c] = max_i |V[b,h,i,c]| / 127 (1 for an all-zero column), computed in fp64 like the reference. */
+int ba_quantize_values(ba_handle* h, const ba_params* p, const void* V, int8_t* vq, double* scales, void* stream);
+
 /* binary_gemm (bitops.cpp:96-131) for ONE head: S[i,j] = d - 2*popc(q_i xor k_j), int32 [N,N].
  * Verification only (the fused kernel never materialises S). */
 int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, const uint64_t* k_words,
                      int64_t head_index, int32_t* S, void* stream);
 
 /* binary_attention_fused (attention.cpp:250-382), quantize_pv = false semantics, for all B*H heads.
- * row_max / row_sum: optional [B,H,N] float32 (AttentionOutput::row_max / row_sum, attention.hpp:45-46). */
+ * row_max / row_sum: optional [B,H,N] float32 (AttentionOutput::row_max / row_sum, attention.hpp:45-46).
+ * quantize_pv = 1 selects the reference's integer P.V mode (attention.cpp:332-343, 361-363). */
 int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
                             const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
                             void* stream);

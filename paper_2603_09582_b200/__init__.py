@@ -7,10 +7,10 @@ Python is only the host-side convenience layer over the C ABI in include/binattn
 a GPU (so the build can be checked), every compute call needs one.
 """
 from .api import (BinaryAttention, BinAttnError, ShapeError, ValidationError, CudaError, UnsupportedError,
-                  binary_attention, binary_attention_fused, AttentionConfig, AttentionOutput, Relative1dBias,
+                  binary_attention, binary_attention_fused, AttentionConfig, AttentionOutput, Relative1dBias, Relative2dBias,
                   load_library)
 from .launcher import shard_range, shard_heads
 
 __all__ = ["BinaryAttention", "BinAttnError", "ShapeError", "ValidationError", "CudaError", "UnsupportedError",
-           "binary_attention", "binary_attention_fused", "AttentionConfig", "AttentionOutput", "Relative1dBias", "load_library",
+           "binary_attention", "binary_attention_fused", "AttentionConfig", "AttentionOutput", "Relative1dBias", "Relative2dBias", "load_library",
            "shard_range", "shard_heads"]

@@ -51,7 +51,8 @@ _STATUS = {1: ShapeError, 2: ValidationError, 3: CudaError, 4: UnsupportedError}
 class _Params(C.Structure):
     _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("N", C.c_int32), ("d", C.c_int32), ("in_dtype", C.c_int32),
                 ("bias_mode", C.c_int32), ("bias_heads", C.c_int32), ("bias_dtype", C.c_int32),
-                ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32)]
+                ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32),
+                ("quantize_pv", C.c_int32), ("block_cols", C.c_int32)]
 
 
 _lib = None
@@ -73,6 +74,7 @@ def load_library() -> C.CDLL:
     lib.ba_workspace_bytes.restype = C.c_size_t
     lib.ba_pack_signs.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp]
     lib.ba_binary_logits.argtypes = [vp, C.POINTER(_Params), vp, vp, i64, vp, vp]
+    lib.ba_quantize_values.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp]
     lib.ba_binary_attention_fwd.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.ba_binary_attention_host.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]
     lib.ba_shard_range.argtypes = [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
@@ -104,10 +106,35 @@ class Relative1dBias:
 
 
 @dataclass
+class Relative2dBias:
+    """binattn::Relative2dBias (attention.hpp:22-26): N = g*g tokens on a g x g grid,
+    b_ij = row_offsets[ri - rj + g - 1] + col_offsets[ci - cj + g - 1], both tables of length 2g-1 (or [1|H, 2g-1]).
+    Expanded on the device to the dense table materialize_bias builds (attention.cpp:78-96) and fed to the dense path."""
+    row_offsets: torch.Tensor
+    col_offsets: torch.Tensor
+
+    def materialize(self, n: int) -> torch.Tensor:
+        g = int(round(math.sqrt(n)))
+        if g * g != n:
+            raise ShapeError("bias: relative-2d requires N to be a perfect square")  # attention.cpp:79-81
+        ro, co = self.row_offsets, self.col_offsets
+        ro = ro.unsqueeze(0) if ro.dim() == 1 else ro
+        co = co.unsqueeze(0) if co.dim() == 1 else co
+        if ro.shape[-1] != 2 * g - 1 or co.shape[-1] != 2 * g - 1 or ro.shape[0] != co.shape[0]:
+            raise ShapeError("bias: relative-2d tables must have length 2*sqrt(N)-1")  # attention.cpp:82-83
+        idx = torch.arange(n, device=ro.device)
+        r, c = idx // g, idx % g
+        dr = r[:, None] - r[None, :] + (g - 1)
+        dc = c[:, None] - c[None, :] + (g - 1)
+        return ro[:, dr] + co[:, dc]  # [Hb, N, N]
+
+
+@dataclass
 class AttentionConfig:
     """binattn::AttentionConfig (attention.hpp:29-41).  block_rows/block_cols are accepted and validated like the
     reference's (attention.cpp:26-28) but do not change the result: the CUDA kernels pick their own tiles and the
-    reference itself is tile-invariant to 1e-12 (test_attention.cpp:254-272).  quantize_pv must be False."""
+    reference itself is tile-invariant to 1e-12 (test_attention.cpp:254-272).  quantize_pv=True runs the integer P.V
+    mode on the CUDA cores, where block_cols (<= 64) DOES shape the result, exactly as in the reference."""
     seq_len: int = 0
     head_dim: int = 0
     temperature: float = 1.0
@@ -154,10 +181,11 @@ class BinaryAttention:
             pass
 
     # ------------------------------------------------------------------------------------------
-    def _params(self, B, H, N, d, dtype, bias=None, scale=None, kernel="auto") -> _Params:
+    def _params(self, B, H, N, d, dtype, bias=None, scale=None, kernel="auto", quantize_pv=False, block_cols=None) -> _Params:
         if dtype not in _DTYPES:
             raise ValidationError(f"unsupported input dtype {dtype}")
         p = _Params(B=B, H=H, N=N, d=d, in_dtype=_DTYPES[dtype], kernel=KERNELS[kernel])
+        p.quantize_pv, p.block_cols = int(bool(quantize_pv)), int(block_cols or 0)
         p.inv_tau = (1.0 / math.sqrt(d)) if scale is None else float(scale)
         if isinstance(bias, Relative1dBias):
             off = bias.offsets
@@ -176,6 +204,8 @@ class BinaryAttention:
         """Shape rules of materialize_bias (attention.cpp:59-67); returns the tensor whose pointer goes to the C ABI."""
         if bias is None:
             return None, None
+        if isinstance(bias, Relative2dBias):
+            bias = bias.materialize(N)
         if isinstance(bias, Relative1dBias):
             off = bias.offsets
             if off.dim() == 1:
@@ -228,6 +258,18 @@ class BinaryAttention:
         _check(self.lib.ba_pack_signs(self.h, C.byref(p), _ptr(X), _ptr(words), _ptr(mu), self._stream()))
         return words, mu
 
+    def quantize_values(self, V: torch.Tensor):
+        """quantize_values for every head (quantize.cpp:57-74): returns (levels int8 [B,H,N,d], scales float64 [B,H,d])."""
+        if V.dim() != 4:
+            raise ShapeError("quantize_values: V must be [B,H,N,d]")
+        V = V.contiguous()
+        B, H, N, d = V.shape
+        vq = torch.empty((B, H, N, d), dtype=torch.int8, device=V.device)
+        sc = torch.empty((B, H, d), dtype=torch.float64, device=V.device)
+        p = self._params(B, H, N, d, V.dtype)
+        _check(self.lib.ba_quantize_values(self.h, C.byref(p), _ptr(V), _ptr(vq), _ptr(sc), self._stream()))
+        return vq, sc
+
     def binary_logits(self, q_words: torch.Tensor, k_words: torch.Tensor, d: int, head: int = 0) -> torch.Tensor:
         """binary_gemm for one head: int32 [N,N] = d - 2*popc(q xor k)."""
         B, H, N, _ = q_words.shape
@@ -237,8 +279,10 @@ class BinaryAttention:
                                          head, _ptr(S), self._stream()))
         return S
 
-    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False):
-        """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output)."""
+    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False, quantize_pv=False, block_cols=None):
+        """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output).
+        quantize_pv=True selects the reference's default u8 x s8 integer P.V mode (attention.hpp:35; CUDA-core kernel);
+        block_cols is that mode's key-block size (default min(64, N), like AttentionConfig::make)."""
         if Q.dim() != 4:
             raise ShapeError("attention: Q must be [B,H,N,d]")
         if K.shape != Q.shape:
@@ -250,7 +294,7 @@ class BinaryAttention:
         B, H, N, d = Q.shape
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
         bias, bias_t = self._check_bias(bias, H, N)
-        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel, quantize_pv, block_cols)
         O = torch.empty((B, H, N, d), dtype=torch.float32, device=Q.device)
         m = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
         l = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
@@ -308,16 +352,16 @@ def binary_attention_fused(q, k, v, cfg: AttentionConfig, with_probs: bool = Fal
         raise ValidationError("attention: temperature must be positive")
     if cfg.block_rows < 1 or cfg.block_rows > n or cfg.block_cols < 1 or cfg.block_cols > n:  # attention.cpp:26-28
         raise ValidationError("attention: block sizes must be in [1, N]")
-    if cfg.quantize_pv:
-        raise UnsupportedError("quantize_pv=true (int8 P.V) is not built; the CUDA path implements quantize_pv=false")
     if with_probs:
         raise UnsupportedError("with_probs is diagnostics-only in the reference and is not carried over")
-    if isinstance(cfg.bias, Relative1dBias):
+    if isinstance(cfg.bias, Relative2dBias):
+        pass  # shape rules are checked when the table is expanded (Relative2dBias.materialize)
+    elif isinstance(cfg.bias, Relative1dBias):
         if cfg.bias.offsets.dim() != 1 or cfg.bias.offsets.shape[0] != 2 * n - 1:
             raise ShapeError("bias: relative-1d offsets must have length 2N-1")  # attention.cpp:66-67
     elif cfg.bias is not None and (cfg.bias.dim() != 2 or cfg.bias.shape[0] != n or cfg.bias.shape[1] != n):
         raise ShapeError("bias: dense table must be N x N")  # attention.cpp:60-61
     ba = _handle_for(q.device)
     O, m, l = ba.forward(q[None, None], k[None, None], v[None, None], cfg.bias, 1.0 / cfg.temperature,
-                         return_stats=True)
+                         return_stats=True, quantize_pv=cfg.quantize_pv, block_cols=cfg.block_cols)
     return AttentionOutput(O[0, 0], m[0, 0], l[0, 0])

@@ -1,0 +1,155 @@
+// attn_int8.cu -- the reference's DEFAULT mode, quantize_pv = true (Algorithm 1 of the paper):
+//   K1v  quantize_values   per-channel s8 levels of V (proj/src/quantize.cpp:57-74): delta[c] = max_i|V[i,c]| / 127
+//                          (1 for an all-zero column), Vq[i,c] = round_half_away(V[i,c] / delta[c])
+//   K2q  fused attention   per key block of block_cols columns (attention.cpp:284-343): block max, m_new, rescale,
+//                          P^ = exp(S - m_new), l = rescale*l + sum P^, O *= rescale, acc(int32) = sum_j round(255 P^_j) * Vq[j,:],
+//                          O += acc; epilogue Y = O / l / 255 * delta[c] (attention.cpp:354-364)
+// CUDA-core, correctness-first implementation: the integer products run on the SIMT pipes, one
+// thread per (query row, 32-column slice of d) like attn_simt.cu.  The result depends on block_cols exactly as the
+// reference's does (the u8 grid of P^ is relative to the running max after each key block), so the same block size must
+// be used on both sides; blocks of up to 64 keys are staged in shared memory.  K1v works in fp64 so that the s8 levels
+// and the scales are bit-identical to the reference's; K2q works in fp32 (a weight that lands within ~1e-5 of a .5
+// rounding boundary may round the other way than in fp64 -- parity is by tolerance, as SURVEY.md 8f says).
+#include "ba_common.cuh"
+
+namespace ba {
+
+constexpr int kQvThreads = 256;
+constexpr int kI8Rows = 64;     // query rows per CTA
+constexpr int kI8Slice = 32;    // O columns per thread
+constexpr int kI8MaxBc = 64;    // keys per block staged in shared memory
+constexpr int kI8MaxW64 = 4;    // d <= 256
+
+// One CTA per head: column abs-max (exact: max is order independent), then the s8 levels.
+__global__ void __launch_bounds__(kQvThreads) quantize_values_kernel(const void* V, int in_dtype, int N, int d, int8_t* vq,
+                                                                     double* scales) {
+    __shared__ unsigned int amax_bits[256];
+    __shared__ double delta[256];
+    const int head = blockIdx.x;
+    const int64_t base = (int64_t)head * N * d;
+    for (int c = threadIdx.x; c < d; c += kQvThreads) amax_bits[c] = 0u;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < N * d; idx += kQvThreads) {
+        const float v = fabsf(load_as_float(V, in_dtype, base + idx));  // non-negative floats order like their bit patterns
+        atomicMax(&amax_bits[idx % d], __float_as_uint(v));
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += kQvThreads) {
+        const double amax = (double)__uint_as_float(amax_bits[c]);
+        const double s = amax > 0.0 ? amax / 127.0 : 1.0;  // quantize.cpp:61-66
+        delta[c] = s;
+        scales[(int64_t)head * d + c] = s;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < N * d; idx += kQvThreads)
+        vq[base + idx] = (int8_t)round((double)load_as_float(V, in_dtype, base + idx) / delta[idx % d]);  // round_half_away
+}
+
+__global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_constant__ FwdArgs a, const int8_t* __restrict__ vq,
+                                                                   const double* __restrict__ scales, int row_blocks, int bc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ns = blockDim.y;           // 32-column slices = ceil(d/32)
+    const int dp = ns * kI8Slice;        // padded head dim in shared memory
+    int8_t* sv = reinterpret_cast<int8_t*>(smem_raw);                                   // [kI8MaxBc][dp]
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kI8MaxBc * dp);       // [kI8MaxBc][W64]
+    const int head = blockIdx.x / row_blocks, rb = blockIdx.x - head * row_blocks;
+    const int tx = threadIdx.x, sl = threadIdx.y;
+    const int tid = sl * kI8Rows + tx, nthreads = kI8Rows * ns;
+    const int row = rb * kI8Rows + tx;
+    const bool row_ok = row < a.N;
+    const int N = a.N, d = a.d, w64 = a.W64;
+
+    uint64_t qb[kI8MaxW64];
+#pragma unroll
+    for (int w = 0; w < kI8MaxW64; ++w) qb[w] = (row_ok && w < w64) ? a.q_words[((int64_t)head * N + row) * w64 + w] : 0ull;
+    const float sc = a.mu_q[head] * a.mu_k[head] * a.inv_tau;  // score = mu_q*mu_k*dot/tau + bias (attention.cpp:34-36)
+    const char* bias_row = nullptr;
+    const bool rel1d = a.bias_kind == BA_BIAS_REL1D;
+    if (a.bias && row_ok) {
+        const int64_t table = (a.head0 + head) % a.H % a.bias_heads;
+        bias_row = static_cast<const char*>(a.bias) +
+                   (rel1d ? table * (2 * (int64_t)N - 1) : (table * N + row) * a.bias_ld) * dtype_size(a.bias_dtype);
+    }
+    auto score = [&](int jj, int j) {  // natural-log units, like the reference
+        int diff = 0;
+#pragma unroll
+        for (int w = 0; w < kI8MaxW64; ++w)
+            if (w < w64) diff += __popcll(qb[w] ^ sk[jj * w64 + w]);
+        float x = (float)(d - 2 * diff) * sc;
+        if (bias_row) x += load_as_float(bias_row, a.bias_dtype, rel1d ? row - j + N - 1 : j);
+        return x;
+    };
+
+    float o[kI8Slice];
+#pragma unroll
+    for (int c = 0; c < kI8Slice; ++c) o[c] = 0.f;
+    float m = -INFINITY, l = 0.f;
+
+    for (int j0 = 0; j0 < N; j0 += bc) {
+        const int nk = min(bc, N - j0);
+        __syncthreads();
+        for (int t = tid; t < nk * w64; t += nthreads) sk[t] = a.k_words[((int64_t)head * N + j0) * w64 + t];
+        for (int t = tid; t < nk * dp; t += nthreads) {
+            const int jj = t / dp, c = t - jj * dp;
+            sv[t] = c < d ? vq[((int64_t)head * N + j0 + jj) * d + c] : (int8_t)0;
+        }
+        __syncthreads();
+        if (!row_ok) continue;
+        float bm = -INFINITY;  // block max (attention.cpp:308-309)
+        for (int jj = 0; jj < nk; ++jj) bm = fmaxf(bm, score(jj, j0 + jj));
+        const float m_new = fmaxf(m, bm);
+        const float rescale = expf(m - m_new);  // exp(-inf) = 0 on the first block
+        int acc[kI8Slice];
+#pragma unroll
+        for (int c = 0; c < kI8Slice; ++c) acc[c] = 0;
+        float rs = 0.f;
+        for (int jj = 0; jj < nk; ++jj) {
+            const float p = expf(score(jj, j0 + jj) - m_new);
+            rs += p;
+            const int p8 = (int)floorf(fmaf(p, 255.0f, 0.5f));  // round_half_away of a non-negative value
+            const int* v32 = reinterpret_cast<const int*>(sv + jj * dp + sl * kI8Slice);
+#pragma unroll
+            for (int c4 = 0; c4 < kI8Slice / 4; ++c4) {
+                const int pk = v32[c4];
+                acc[4 * c4 + 0] += p8 * (int)(int8_t)(pk & 0xFF);
+                acc[4 * c4 + 1] += p8 * (int)(int8_t)((pk >> 8) & 0xFF);
+                acc[4 * c4 + 2] += p8 * (int)(int8_t)((pk >> 16) & 0xFF);
+                acc[4 * c4 + 3] += p8 * (int)(int8_t)(pk >> 24);
+            }
+        }
+        l = rescale * l + rs;
+        m = m_new;
+#pragma unroll
+        for (int c = 0; c < kI8Slice; ++c) o[c] = o[c] * rescale + (float)acc[c];
+    }
+    if (!row_ok) return;
+    float* orow = a.O + ((int64_t)head * N + row) * d + sl * kI8Slice;
+#pragma unroll
+    for (int c = 0; c < kI8Slice; ++c)
+        if (sl * kI8Slice + c < d) orow[c] = o[c] / l / 255.0f * (float)scales[(int64_t)head * d + sl * kI8Slice + c];
+    if (sl == 0) {
+        if (a.row_max) a.row_max[(int64_t)head * N + row] = m;
+        if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l;
+    }
+}
+
+int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, double* scales,
+                           cudaStream_t stream) {
+    if (d > 256) return -(int)cudaErrorInvalidValue;
+    quantize_values_kernel<<<(unsigned)heads, kQvThreads, 0, stream>>>(V, in_dtype, N, d, vq, scales);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream) {
+    const int ns = (a.d + kI8Slice - 1) / kI8Slice;
+    if (ns > 8 || a.W64 > kI8MaxW64 || block_cols < 1 || block_cols > kI8MaxBc) return -(int)cudaErrorInvalidValue;
+    const int row_blocks = (a.N + kI8Rows - 1) / kI8Rows;
+    const dim3 block(kI8Rows, ns);
+    const size_t smem = (size_t)kI8MaxBc * ns * kI8Slice + sizeof(uint64_t) * kI8MaxBc * a.W64;
+    attn_int8_kernel<<<(unsigned)(a.BH * row_blocks), block, smem, stream>>>(a, vq, scales, row_blocks, block_cols);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
+}  // namespace ba

@@ -41,6 +41,9 @@ int launch_pack_signs(const void* X, int in_dtype, int64_t heads, int N, int d, 
 int pack_partials_per_head(int N, int d, int in_dtype);
 int launch_binary_logits(const uint64_t* qw, const uint64_t* kw, int N, int d, int32_t* S, cudaStream_t stream);
 int launch_attn_simt(const FwdArgs& a, cudaStream_t stream);
+int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, double* scales,
+                           cudaStream_t stream);
+int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream);
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
 bool tcgen05_supported(const ba_params* p, const char** why);
 

@@ -39,7 +39,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    size_t q_words, k_words, mu_q, mu_k, partials, total;
+    size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, total;
     int64_t BH;
     int W64, chunks;
 };
@@ -56,6 +56,11 @@ Layout make_layout(const ba_params* p, int64_t heads = -1) {
     L.mu_q = off; off += align_up((size_t)L.BH * sizeof(float), 256);
     L.mu_k = off; off += align_up((size_t)L.BH * sizeof(float), 256);
     L.partials = off; off += align_up(2 * (size_t)L.BH * L.chunks * sizeof(float), 256);
+    L.vq = L.vscales = off;
+    if (p->quantize_pv) {  // s8 levels of V and their per-channel fp64 scales (quantize_values)
+        L.vq = off; off += align_up((size_t)L.BH * p->N * p->d, 256);
+        L.vscales = off; off += align_up((size_t)L.BH * p->d * sizeof(double), 256);
+    }
     L.total = off;
     return L;
 }
@@ -86,6 +91,12 @@ int check_params(const ba_params* p, bool need_attention) {
             return fail(BA_ERR_VALIDATION, "bias_dtype must be BA_BF16 or BA_F32");
     }
     if (p->d > 256) return fail(BA_ERR_UNSUPPORTED, "head dim %d > 256 is not supported", p->d);
+    if (p->quantize_pv) {
+        const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
+        if (bc < 1 || bc > p->N)  // attention.cpp:26-28
+            return fail(BA_ERR_VALIDATION, "attention: block sizes must be in [1, N]");
+        if (bc > 64) return fail(BA_ERR_UNSUPPORTED, "quantize_pv: block_cols %d > 64 is not supported", bc);
+    }
     return BA_OK;
 }
 
@@ -246,6 +257,7 @@ int ba_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* 
 
 int ba_select_kernel(const ba_params* p) {
     if (check_params(p, true) != BA_OK) return -1;
+    if (p->quantize_pv) return p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT;
     const char* why = nullptr;
     if (p->kernel == BA_KERNEL_SIMT) return BA_KERNEL_SIMT;
     return ba::tcgen05_supported(p, &why) ? BA_KERNEL_TCGEN05 : (p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT);
@@ -267,6 +279,20 @@ int ba_pack_signs(ba_handle* h, const ba_params* p, const void* X, uint64_t* wor
     const int n = ba::launch_pack_signs(X, p->in_dtype, L.BH, p->N, p->d, words, mu, h->partials, h->tickets,
                                         static_cast<cudaStream_t>(stream));
     if (n < 0) return fail(BA_ERR_CUDA, "pack_signs launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+    h->launches += n;
+    return BA_OK;
+}
+
+int ba_quantize_values(ba_handle* h, const ba_params* p, const void* V, int8_t* vq, double* scales, void* stream) {
+    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
+    int rc = check_params(p, false);
+    if (rc) return rc;
+    if (!V || !vq || !scales) return fail(BA_ERR_SHAPE, "quantize_values: V, vq and scales must be non-NULL");
+    if (p->d > 256) return fail(BA_ERR_UNSUPPORTED, "head dim %d > 256 is not supported", p->d);
+    BA_CUDA(cudaSetDevice(h->device));
+    const int n = ba::launch_quantize_values(V, p->in_dtype, (int64_t)p->B * p->H, p->N, p->d, vq, scales,
+                                             static_cast<cudaStream_t>(stream));
+    if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
     return BA_OK;
 }
@@ -326,7 +352,16 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     if (n < 0) return fail(BA_ERR_CUDA, "pack_signs launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
     if (prof) BA_CUDA(cudaEventRecord(ev[1], stream));
-    n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tcgen05(a, stream) : ba::launch_attn_simt(a, stream);
+    if (p->quantize_pv) {  // the reference's default mode: s8 V levels (K1v), then the integer P.V kernel
+        int8_t* vq = reinterpret_cast<int8_t*>(ws + L.vq);
+        double* vs = reinterpret_cast<double*>(ws + L.vscales);
+        n = ba::launch_quantize_values(V, p->in_dtype, heads, p->N, p->d, vq, vs, stream);
+        if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+        h->launches += n;
+        n = ba::launch_attn_int8(a, vq, vs, p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64), stream);
+    } else {
+        n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tcgen05(a, stream) : ba::launch_attn_simt(a, stream);
+    }
     if (n < 0) return fail(BA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
     if (prof) {
@@ -340,6 +375,11 @@ static int resolve_kernel(const ba_params* p, int* kernel) {
     const char* why = "";
     const bool tc_ok = ba::tcgen05_supported(p, &why);
     int k = p->kernel;
+    if (p->quantize_pv) {  // integer P.V runs on the CUDA cores only (for now)
+        if (k == BA_KERNEL_TCGEN05) return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 has no tcgen05 kernel yet");
+        *kernel = BA_KERNEL_SIMT;
+        return BA_OK;
+    }
     if (k == BA_KERNEL_AUTO) k = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
     if (k == BA_KERNEL_TCGEN05 && !tc_ok) return fail(BA_ERR_UNSUPPORTED, "tcgen05 kernel: %s", why);
     if (k != BA_KERNEL_TCGEN05 && k != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");

@@ -134,6 +134,27 @@ int main() {
             for (std::size_t i = 0; i < c.n * c.d; ++i) CHECK(o2.data().data()[i] == out.output.data().data()[i]);
         }
     }
+    {  // quantize_pv = true, the reference's default mode (attention.hpp:35; test_attention.cpp:300-314 shape: N=64 d=32, 16x16)
+        for (Precision prec : {Precision::f32, Precision::bf16}) {
+            const std::size_t n = 64, d = 32;
+            bo_rng_init(rng.data(), 40, 0);
+            const Mat q = rounded(random_dense(rng.data(), n, d), prec), k = rounded(random_dense(rng.data(), n, d), prec),
+                      v = rounded(random_dense(rng.data(), n, d), prec);
+            Cfg cfg = Cfg::make(n, d);
+            cfg.precision = prec;
+            cfg.quantize_pv = true;
+            cfg.block_rows = 16;
+            cfg.block_cols = 16;
+            const auto out = eng.binary_attention_fused(q, k, v, cfg);
+            std::vector<double> y(n * d), m(n), l(n);
+            CHECK(bo_binary_attention_fused(q.data().data(), k.data().data(), v.data().data(), n, d, cfg.temperature, 16, 16, 1,
+                                            nullptr, y.data(), m.data(), l.data()) == 0);
+            double worst = 0.0;
+            for (std::size_t i = 0; i < n * d; ++i) worst = std::fmax(worst, std::fabs(out.output.data().data()[i] - y[i]));
+            std::printf("quantize_pv=true N=%zu d=%zu %s  max_abs=%.3e\n", n, d, prec == Precision::bf16 ? "bf16" : "f32", worst);
+            CHECK(worst <= 1e-3);
+        }
+    }
     {  // Relative1dBias (attention.hpp:18-21, attention.cpp:65-76): offsets handed to the kernels, table built for the oracle
         for (Precision prec : {Precision::f32, Precision::bf16}) {
             const std::size_t n = 197, d = 64;

@@ -307,6 +307,77 @@ def test_relative_1d_bias_generated_in_kernel(ba, port, n, d, per_head):
         ba.forward(Q, K, V, pkg.Relative1dBias(torch.zeros(2 * n, device="cuda")))
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("n,d", [(197, 64), (256, 72), (64, 32), (50, 12), (130, 128)])
+def test_quantize_values_bit_exact(ba, port, n, d, dtype):
+    """K1v vs quantize_values (quantize.cpp:57-74): s8 levels identical, fp64 scales identical; never -128, a zero column
+    gets scale 1 (test_quantize.cpp:99-138)."""
+    import torch
+    heads = [make_head_inputs(port, 44, s, n, d, dtype=dtype)[2] for s in range(2)]
+    heads[1] = heads[1].copy()
+    heads[1][:, 3] = 0.0  # all-zero column
+    vq, sc = ba.quantize_values(to_torch(np.stack(heads)[None], dtype))
+    for h in range(2):
+        oq, os_ = port.quantize_values(heads[h])
+        assert np.array_equal(vq[0, h].cpu().numpy(), oq)
+        assert np.array_equal(sc[0, h].cpu().numpy(), os_)
+    assert int(vq.min()) >= -127 and float(sc[0, 1, 3]) == 1.0
+
+
+@pytest.mark.parametrize("bias_mode", [None, "per_head"])
+@pytest.mark.parametrize("n,d,bc", [(197, 64, None), (256, 72, None), (64, 32, 16), (130, 128, 64), (48, 16, 5), (300, 72, 33)])
+def test_int8_pv_mode_matches_reference_default(ba, port, n, d, bc, bias_mode):
+    """quantize_pv = true, the reference's DEFAULT mode (attention.hpp:35, attention.cpp:332-343, 361-363): same key-block
+    size on both sides.  fp32 exp against fp64 exp can flip round(255 P^) at a .5 boundary (one level = 1/255 of a weight),
+    hence a tolerance; the reference's own bound for this mode against its fp64 path is rel-L2 1e-2
+    (test_attention.cpp:300-314), which must hold here too."""
+    heads = [make_head_inputs(port, 45, s, n, d, bias_scale=0.5 if bias_mode else None) for s in range(2)]
+    Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
+    bias_t = to_torch(np.stack([h[3] for h in heads]), "bf16") if bias_mode else None
+    O, m, l = ba.forward(Q, K, V, bias_t, quantize_pv=True, block_cols=bc, return_stats=True)
+    O = O.cpu().numpy().astype(np.float64)
+    for h in range(2):
+        q, k, v, b = heads[h]
+        y8, om, ol = port.binary_attention_fused(q, k, v, bias=b, quantize_pv=True, block_cols=bc)
+        assert np.abs(O[0, h] - y8).max() <= 1e-3, np.abs(O[0, h] - y8).max()
+        np.testing.assert_allclose(m[0, h].cpu().numpy(), om, rtol=0, atol=1e-4)
+        np.testing.assert_allclose(l[0, h].cpu().numpy(), ol, rtol=2e-5)
+        y64 = port.binary_attention_fused(q, k, v, bias=b)[0]
+        assert np.linalg.norm(O[0, h] - y64) / np.linalg.norm(y64) <= 1e-2
+
+
+def test_int8_pv_mode_errors(ba):
+    import torch
+    import paper_2603_09582_b200 as pkg
+    q = torch.zeros(1, 1, 100, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(pkg.ValidationError):  # attention.cpp:26-28
+        ba.forward(q, q, q, quantize_pv=True, block_cols=101)
+    with pytest.raises(pkg.UnsupportedError):
+        ba.forward(q, q, q, quantize_pv=True, block_cols=80)
+    with pytest.raises(pkg.UnsupportedError):
+        ba.forward(q, q, q, quantize_pv=True, kernel="tcgen05")
+
+
+def test_relative_2d_bias(ba, port):
+    """Relative2dBias (attention.hpp:22-26, attention.cpp:78-96): expanded on the device, checked against the oracle fed
+    the reference's own materialize_bias table; a non-square N is a ShapeError like the reference's."""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    n, d, g = 256, 64, 16
+    q, k, v, _ = make_head_inputs(port, 43, 0, n, d)
+    rng = np.random.default_rng(9)
+    ro, co = (cpu.bf16_round(0.5 * rng.standard_normal(2 * g - 1)) for _ in range(2))
+    table = port.bias_rel2d(ro, co, n)
+    Q, K, V = (to_torch(x[None, None], "bf16") for x in (q, k, v))
+    rel = pkg.Relative2dBias(to_torch(ro, "f32"), to_torch(co, "f32"))
+    assert np.array_equal(rel.materialize(n)[0].cpu().numpy().astype(np.float64), table)
+    O = ba.forward(Q, K, V, rel)
+    y = port.binary_attention_fused(q, k, v, bias=table)[0]
+    assert np.abs(O[0, 0].cpu().numpy().astype(np.float64) - y).max() <= TOL_O
+    with pytest.raises(pkg.ShapeError):
+        ba.forward(Q[:, :, :200], K[:, :, :200], V[:, :, :200], rel)
+
+
 def test_torch_library_op(ba, port):
     """torch.ops.binattn.binary_attention / _rel1d: same bytes as the handle API, and traceable through the fake kernel."""
     import torch
