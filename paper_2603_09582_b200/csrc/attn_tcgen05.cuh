@@ -924,7 +924,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             constexpr int W = (KPAD + 63) / 64;
             constexpr int NF = FOLD ? kFoldMax : 1;
             uint64_t fq[W], fk[NF][W];
-            float fb[NF];
+            float fb[NF];                       // BIAS 2: values; BIAS 1: unused (the raw 16-byte vector fbraw is unpacked at use --
+            uint4 fbraw = make_uint4(0, 0, 0, 0);  // converting here would stall this in-order thread on the load)
             if (FOLD && warp_ok) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) fq[w] = (row_ok && w < w64) ? __ldg(a.q_words + ((int64_t)head * N + row) * w64 + w) : 0ull;
@@ -939,13 +940,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     const char* brow_g = static_cast<const char*>(a.bias) +
                                          ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
                     if (BIAS == 1) {  // bf16 rows padded to 16 bytes: the 8 columns after the last full tile are one vector
-                        const uint4 b = __ldg(reinterpret_cast<const uint4*>(brow_g + (size_t)T * BN * 2));
-                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-                        for (int e = 0; e < NF / 2; ++e) {
-                            fb[2 * e] = __uint_as_float(bw[e] << 16);
-                            fb[2 * e + 1] = __uint_as_float(bw[e] & 0xFFFF0000u);
-                        }
+                        fbraw = __ldg(reinterpret_cast<const uint4*>(brow_g + (size_t)T * BN * 2));
                     } else {
 #pragma unroll
                         for (int i = 0; i < NF; ++i)
@@ -990,6 +985,23 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                     for (int i = 0; i < kFoldMax; ++i) xt[i] = -INFINITY;
                     if (FOLD && j == T - 1) {  // logits of the folded keys: d - 2*popc(q xor k) (bitops.cpp:59-67)
                         nt = prm.fold;
+                        // pin the use of the prefetched words to this tile: the logits below do not depend on j, so the
+                        // compiler would otherwise hoist them to the unit header and stall there on the loads
+#pragma unroll
+                        for (int w = 0; w < W; ++w) asm volatile("" : "+l"(fq[w]));
+#pragma unroll
+                        for (int i = 0; i < NF; ++i)
+#pragma unroll
+                            for (int w = 0; w < W; ++w) asm volatile("" : "+l"(fk[i][w]));
+                        asm volatile("" : "+r"(fbraw.x), "+r"(fbraw.y), "+r"(fbraw.z), "+r"(fbraw.w));
+                        if (BIAS == 1) {
+                            const uint32_t bw[4] = {fbraw.x, fbraw.y, fbraw.z, fbraw.w};
+#pragma unroll
+                            for (int e = 0; e < NF / 2; ++e) {
+                                fb[2 * e] = __uint_as_float(bw[e] << 16);
+                                fb[2 * e + 1] = __uint_as_float(bw[e] & 0xFFFF0000u);
+                            }
+                        }
 #pragma unroll
                         for (int i = 0; i < NF; ++i) {
                             int pc = 0;
