@@ -45,7 +45,8 @@ constexpr int kMaxStages = 4;
 constexpr int kRelWin = 200;        // floats of the relative-1d bias window of one tile: 8 (folded keys) + 128 + 64 - 1, padded
 constexpr int kRelStage = 1024;    // bytes of one window stage
 constexpr int kFoldMax = 8;        // trailing keys that can be folded into the last full tile (CUDA-core logits, 5th P.V k-step)
-constexpr int kRegsSoftmax = 200, kRegsCtrl = 56;  // setmaxnreg split of the 2 x 128 x 128 register pool
+constexpr int kRegsSoftmax = 200, kRegsCtrl = 56;  // setmaxnreg split of the 2 x 128 x 128 register pool (folded-tail kernels;
+                                                  // the others run 192 / 64, which is what keeps each side free of spills)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kSuspendHint = 0x989680;  // try_wait may sleep this long before re-polling (cuts spin instructions)
 
@@ -687,7 +688,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     // register rebalancing between the two warpgroups (the pool is 256 x 128 per CTA): the softmax threads hold a
     // 64-column score row plus the bias row, the control warps need very little
     if (warp >= 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtrl));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(MODE == 1 ? kRegsCtrl : kRegsCtrl + 8));
     if (warp == 4) {
         // ============================================================ MMA issuer (whole warp, uniform control flow)
         // instruction descriptors (cute::UMMA::InstrDescriptor bit layout)
@@ -868,7 +869,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         }
     }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MODE == 1 ? kRegsSoftmax : kRegsSoftmax - 8));
         // ============================================================ softmax + epilogue (thread = query row)
         const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
         Ring br;
