@@ -50,8 +50,11 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ns = blockDim.y;           // 32-column slices = ceil(d/32)
     const int dp = ns * kI8Slice;        // padded head dim in shared memory
-    int8_t* sv = reinterpret_cast<int8_t*>(smem_raw);                                   // [kI8MaxBc][dp]
+    // s8 V levels of the key block, four consecutive keys of one column per 32-bit word ([kI8MaxBc/4][dp] words), so one
+    // dp4a.u32.s32 multiplies four u8 weights with four s8 levels of a column (exact in int32, like the reference's loop)
+    uint32_t* sv4 = reinterpret_cast<uint32_t*>(smem_raw);
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kI8MaxBc * dp);       // [kI8MaxBc][W64]
+    int8_t* sv = reinterpret_cast<int8_t*>(smem_raw);
     const int head = blockIdx.x / row_blocks, rb = blockIdx.x - head * row_blocks;
     const int tx = threadIdx.x, sl = threadIdx.y;
     const int tid = sl * kI8Rows + tx, nthreads = kI8Rows * ns;
@@ -89,9 +92,9 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
         const int nk = min(bc, N - j0);
         __syncthreads();
         for (int t = tid; t < nk * w64; t += nthreads) sk[t] = a.k_words[((int64_t)head * N + j0) * w64 + t];
-        for (int t = tid; t < nk * dp; t += nthreads) {
+        for (int t = tid; t < ((nk + 3) / 4 * 4) * dp; t += nthreads) {  // byte (jj, c) lives at ((jj/4)*dp + c)*4 + jj%4
             const int jj = t / dp, c = t - jj * dp;
-            sv[t] = c < d ? vq[((int64_t)head * N + j0 + jj) * d + c] : (int8_t)0;
+            sv[((jj >> 2) * dp + c) * 4 + (jj & 3)] = (jj < nk && c < d) ? vq[((int64_t)head * N + j0 + jj) * d + c] : (int8_t)0;
         }
         __syncthreads();
         if (!row_ok) continue;
@@ -103,19 +106,20 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
 #pragma unroll
         for (int c = 0; c < kI8Slice; ++c) acc[c] = 0;
         float rs = 0.f;
-        for (int jj = 0; jj < nk; ++jj) {
-            const float p = expf(score(jj, j0 + jj) - m_new);
-            rs += p;
-            const int p8 = (int)floorf(fmaf(p, 255.0f, 0.5f));  // round_half_away of a non-negative value
-            const int* v32 = reinterpret_cast<const int*>(sv + jj * dp + sl * kI8Slice);
+        for (int j4 = 0; j4 < nk; j4 += 4) {
+            uint32_t p4 = 0;  // four u8 weights, key j4 in the low byte (zero past the block)
 #pragma unroll
-            for (int c4 = 0; c4 < kI8Slice / 4; ++c4) {
-                const int pk = v32[c4];
-                acc[4 * c4 + 0] += p8 * (int)(int8_t)(pk & 0xFF);
-                acc[4 * c4 + 1] += p8 * (int)(int8_t)((pk >> 8) & 0xFF);
-                acc[4 * c4 + 2] += p8 * (int)(int8_t)((pk >> 16) & 0xFF);
-                acc[4 * c4 + 3] += p8 * (int)(int8_t)(pk >> 24);
+            for (int e = 0; e < 4; ++e) {
+                if (j4 + e < nk) {
+                    const float p = expf(score(j4 + e, j0 + j4 + e) - m_new);
+                    rs += p;
+                    p4 |= (uint32_t)floorf(fmaf(p, 255.0f, 0.5f)) << (8 * e);  // round_half_away of a non-negative value
+                }
             }
+            const uint32_t* v4 = sv4 + (j4 >> 2) * dp + sl * kI8Slice;
+#pragma unroll
+            for (int c = 0; c < kI8Slice; ++c)
+                asm("dp4a.u32.s32 %0, %1, %2, %0;" : "+r"(acc[c]) : "r"(p4), "r"(v4[c]));
         }
         l = rescale * l + rs;
         m = m_new;
@@ -146,7 +150,7 @@ int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, i
     if (ns > 8 || a.W64 > kI8MaxW64 || block_cols < 1 || block_cols > kI8MaxBc) return -(int)cudaErrorInvalidValue;
     const int row_blocks = (a.N + kI8Rows - 1) / kI8Rows;
     const dim3 block(kI8Rows, ns);
-    const size_t smem = (size_t)kI8MaxBc * ns * kI8Slice + sizeof(uint64_t) * kI8MaxBc * a.W64;
+    const size_t smem = (size_t)kI8MaxBc * ns * kI8Slice + sizeof(uint64_t) * kI8MaxBc * a.W64;  // s8 tile + packed K words
     attn_int8_kernel<<<(unsigned)(a.BH * row_blocks), block, smem, stream>>>(a, vq, scales, row_blocks, block_cols);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
