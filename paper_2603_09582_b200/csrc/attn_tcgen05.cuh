@@ -900,24 +900,37 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             BA_TMEM_LD16(lane_base + kColS + 32, x, 32);
             BA_TMEM_LD16(lane_base + kColS + 48, x, 48);
         }
+        // (head, query block, bias table) of the unit are carried incrementally: this thread is alone on its critical
+        // path, and the divisions / modulos of a fresh decomposition cost several hundred cycles per unit
+        const int step_h = G / prm.mblocks, step_m = G - step_h * prm.mblocks;
+        int head = (int)blockIdx.x / prm.mblocks, mb = (int)blockIdx.x - head * prm.mblocks;
+        int tab = (a.head0 + head) % a.H;             // head index inside the batch element
+        const int step_t = step_h % a.H;
         for (int u = blockIdx.x; u < prm.units; u += G) {
-            const int head = u / prm.mblocks;
-            const int row0 = (u - head * prm.mblocks) * BM;
+            const int row0 = mb * BM;
             const int row = row0 + tid;
             const bool row_ok = row < N;
             const bool warp_ok = row0 + warp * 32 < N;  // warps whose 32 rows are all past N only keep the barriers moving
+            const int bias_tab = a.bias_heads == 1 ? 0 : tab;  // bias_heads is 1 or H
             const float sc = muq_next * muk_next * a.inv_tau;  // natural-log units per unit of dot
+            // next unit of this CTA
+            int head_n = head + step_h, mb_n = mb + step_m, tab_n = tab + step_t;
+            if (mb_n >= prm.mblocks) {
+                mb_n -= prm.mblocks;
+                ++head_n;
+                ++tab_n;
+            }
+            if (tab_n >= a.H) tab_n -= a.H;
+            if (tab_n >= a.H) tab_n -= a.H;
             if (u + G < prm.units) {
-                const int hn = (u + G) / prm.mblocks;
-                muq_next = __ldg(a.mu_q + hn);
-                muk_next = __ldg(a.mu_k + hn);
+                muq_next = __ldg(a.mu_q + head_n);
+                muk_next = __ldg(a.mu_k + head_n);
             }
             // BIAS == 0 keeps x = raw integer dot and folds sc*log2e into the exponent FMA; otherwise x = dot*sc + bias
             const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;
             const char* bias_row = nullptr;
             if (BIAS == 2 && row_ok)
-                bias_row = static_cast<const char*>(a.bias) +
-                           ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                bias_row = static_cast<const char*>(a.bias) + ((int64_t)bias_tab * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
             RowState rs{-INFINITY, -INFINITY, 0.f};
             const bool dump = DBG && prm.dbg_S && head == prm.dbg_head && row_ok;
             // folded tail keys (prm.fold of them): this row's packed query and those keys' packed words / bias values are
@@ -929,17 +942,16 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             uint4 fbraw = make_uint4(0, 0, 0, 0);  // converting here would stall this in-order thread on the load)
             if (FOLD && warp_ok) {
 #pragma unroll
-                for (int w = 0; w < W; ++w) fq[w] = (row_ok && w < w64) ? __ldg(a.q_words + ((int64_t)head * N + row) * w64 + w) : 0ull;
+                for (int w = 0; w < W; ++w) fq[w] = (row_ok && w < w64) ? __ldg(a.q_words + (uint32_t)((head * N + row) * w64 + w)) : 0ull;
 #pragma unroll
                 for (int i = 0; i < NF; ++i) {
 #pragma unroll
                     for (int w = 0; w < W; ++w)
-                        fk[i][w] = (i < prm.fold && w < w64) ? __ldg(a.k_words + ((int64_t)head * N + T * BN + i) * w64 + w) : 0ull;
+                        fk[i][w] = (i < prm.fold && w < w64) ? __ldg(a.k_words + (uint32_t)((head * N + T * BN + i) * w64 + w)) : 0ull;
                     fb[i] = 0.f;
                 }
                 if ((BIAS == 1 || BIAS == 2) && row_ok) {
-                    const char* brow_g = static_cast<const char*>(a.bias) +
-                                         ((int64_t)((a.head0 + head) % a.H % a.bias_heads) * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
+                    const char* brow_g = static_cast<const char*>(a.bias) + ((int64_t)bias_tab * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
                     if (BIAS == 1) {  // bf16 rows padded to 16 bytes: the 8 columns after the last full tile are one vector
                         fbraw = __ldg(reinterpret_cast<const uint4*>(brow_g + (size_t)T * BN * 2));
                     } else {
@@ -1053,6 +1065,9 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             ep.row = row;
             ep.g_last = g - 1;
             ep.rs = rs;
+            head = head_n;
+            mb = mb_n;
+            tab = tab_n;
         }
         if (ep.pending) run_epilogue<ROWSUM>(sm, prm, &omap, sO, ep, lane_base, warp, lane);
         if (prm.o_stage && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem may be released
