@@ -551,16 +551,16 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
         tc_fence_after();
         float l = ep.rs.l;
         float* orow = a.O + ((int64_t)ep.head * a.N + ep.row) * a.d;
-        if (prm.o_stage) {
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // both boxes are free again
-            __syncwarp();
-        }
         for (int c = 0; c < prm.dvp; c += 32) {
             float o[32], den[16];
             const bool two = c + 16 < prm.dvp;
             if (ROWSUM && c == 0) BA_TMEM_LD16(lane_base + kColO + prm.dvp, den, 0);
             BA_TMEM_LD16(lane_base + kColO + c, o, 0);
             if (two) BA_TMEM_LD16(lane_base + kColO + c + 16, o, 16);
+            if (prm.o_stage && c == 0) {  // both staging boxes are free again (their stores were issued a unit ago);
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // overlaps the TMEM loads
+                __syncwarp();
+            }
             tc_wait_ld();
             if (ROWSUM && c == 0) l = den[0];  // sum of the bf16 weights the MMA used (first column of the ones block)
             const float inv_l = 1.0f / l;
@@ -569,19 +569,22 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
             if (prm.o_stage) {
                 const int bi = (c >> 5) & 1;
                 unsigned char* box = stage + (warp * 2 + bi) * 4096;
-                if (c >= 64) {  // third and later boxes of a wide head reuse a buffer inside the same epilogue
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                if (c >= 64 && bi == 0) {  // a wide head reuses the two boxes inside the same epilogue
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
                 }
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     *reinterpret_cast<float4*>(box + lane * 128 + ((q ^ (lane & 7)) << 4)) =
                         make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_3d(omap, box, c, ep.row - lane, ep.head);
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                if (bi == 1 || c + 32 >= prm.dvp) {  // one proxy fence and one bulk group per pair of boxes
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (bi == 1) tma_store_3d(omap, box - 4096, c - 32, ep.row - lane, ep.head);
+                        tma_store_3d(omap, box, c, ep.row - lane, ep.head);
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
                 }
             } else if (ep.row_ok) {
 #pragma unroll
@@ -964,7 +967,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
 
             for (int j = 0; j < T; ++j, ++g) {
                 const uint32_t s = g & 1u;
-                const int nk = min(BN, N - j * BN);
+                const int nk = MODE != 0 ? BN : min(BN, N - j * BN);  // (folded / exact-multiple kernels only see full tiles)
                 const bool has_next = g + 1 < total_tiles;
                 const uint32_t next_addr = lane_base + kColS + (s ^ 1u) * BN;
                 uint64_t* next_bar = &sm->sfull[s ^ 1u];
