@@ -283,7 +283,6 @@ def main():
     if rank == 0:
         sampler.start()
         time.sleep(0.25)
-    ba.profile_begin(args.steps)
     launches0 = ba.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -294,6 +293,13 @@ def main():
     barrier()
     launches = ba.launch_count - launches0
     total_ms = e0.elapsed_time(e1)
+    # per-kernel durations for the roofline: a second pass of the same steps with CUDA events recorded by the C ABI on
+    # the launching stream between K1 and K2 (kept out of the timed region above: an event between the two kernels
+    # defeats the programmatic dependent launch that overlaps K2's prologue with K1's tail, ~2-8 % of a step)
+    ba.profile_begin(args.steps)
+    for _ in range(args.steps):
+        O = ba.forward(Q, K, V, bias, kernel=kernel)
+    torch.cuda.synchronize()
     calls, pack_ms, attn_ms = ba.profile_end()
     clocks = sampler.stop() if rank == 0 else None
 

@@ -687,6 +687,9 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm->tmem_base;
+    // Programmatic dependent launch: everything above (barriers, TMEM, table) ran while K1 was still draining; K1's packed
+    // words and scales are only read from here on.  (A no-op when the kernel was not launched as a dependent.)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     BA_STAMP(tid == 0 ? 0 : tid == 128 ? 1 : tid == 160 ? 2 : 3);
     // register rebalancing between the two warpgroups (the pool is 256 x 128 per CTA): the softmax threads hold a
     // 64-column score row plus the bias row, the control warps need very little
@@ -1130,8 +1133,17 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
     const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
-    attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL><<<grid, kThreads, smem_bytes(prm, KPAD), stream>>>(prm, m.v, m.b, m.o, m.v16);
-    const cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_bytes(prm, KPAD);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap this kernel's prologue with K1's tail
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL>, prm, m.v, m.b, m.o, m.v16);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 

@@ -155,6 +155,7 @@ __device__ __forceinline__ void finish_head_sum(float acc, const PackJob& job, i
 // Fast path: (d * sizeof(T)) % 16 == 0 and X 16-byte aligned.
 template <typename T>
 __global__ void __launch_bounds__(kPackThreads) pack_signs_vec_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int chunks) {
+    asm volatile("griddepcontrol.launch_dependents;");  // see pack_signs_bf16_kernel
     constexpr int EPV = Vec16<T>::kElems;  // elements per 16-byte vector
     constexpr int LPG = 64 / EPV;          // lanes per u64 output word
     constexpr int HALF = LPG / 2;          // lanes per 32-bit half
@@ -242,6 +243,7 @@ __device__ __forceinline__ uint4 ldg_nc_16_pred(const void* p, bool pred) {
 
 template <int VPRP>
 __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int chunks) {
+    asm volatile("griddepcontrol.launch_dependents;");   // K2's CTAs may start their prologue as this grid drains (PDL)
     constexpr int W64 = VPRP / 8;                        // u64 words per row (one lane slot = 8 bf16 = one byte of signs)
     constexpr int ROWS_PER_PASS = kPackThreads / VPRP;   // rows one pass of the CTA covers
     const PackJob& job = jobs.job[blockIdx.z];
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
 // Generic path: any d, any alignment; one thread per (row, u64 word), scalar loads.
 __global__ void __launch_bounds__(kPackThreads) pack_signs_generic_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int dtype,
                                                                           int chunks) {
+    asm volatile("griddepcontrol.launch_dependents;");  // see pack_signs_bf16_kernel
     const PackJob& job = jobs.job[blockIdx.z];
     const int head = blockIdx.x, chunk = blockIdx.y;
     const int w64 = (d + 63) / 64;
