@@ -263,6 +263,8 @@ struct Smem {
     uint64_t pfull[2];                              // P tile written to TMEM by the four softmax warps
     uint64_t pvdone[2];                             // P.V MMA of a tile retired (O and the denominators are up to date)
     uint64_t ofree;                                 // O of the finished unit read out by the four softmax warps
+    uint64_t ffull[2], ffree[2];                    // packed words of the folded tail keys staged / read out (by unit parity)
+    uint64_t kbits[2][kFoldMax][2];                 // those words: [unit parity][key][64-bit word]
     uint2 lut[256];                                 // byte of sign bits -> 8 e4m3 +-1.0 bytes
     uint32_t tmem_base;
 };
@@ -667,6 +669,10 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             mbar_init(&sm->bfree[s], 4);     // one elected arrival per softmax warp (bias stage read out)
         }
         mbar_init(&sm->ofree, 4);            // one elected arrival per softmax warp (O read out by the epilogue)
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm->ffull[s], 1);     // the first expander warp (it owns keys 0..7 past the last full tile)
+            mbar_init(&sm->ffree[s], 4);     // one elected arrival per softmax warp
+        }
         fence_barrier_init();
     }
     if (warp == 4) {
@@ -806,11 +812,14 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     } else if (warp >= 6) {
         // ============================================================ Q / K expanders
         const int t = tid - 6 * 32;  // 0..63: key t of every K tile, query rows t and t + 64 of every Q tile
-        Ring qr, kr, wr;
+        Ring qr, kr, wr, fr;
         uint32_t wq0[KPAD / 32], wq1[KPAD / 32], wk[KPAD / 32];
+        uint32_t wf[FOLD ? KPAD / 32 : 1];  // folded tail: thread t < fold holds the packed words of key T*64 + t
         if ((int)blockIdx.x < prm.units) {  // words of the first unit
             const int head = blockIdx.x / prm.mblocks;
             const int row0 = (blockIdx.x - head * prm.mblocks) * BM;
+            if constexpr (FOLD)
+                if (warp == 6) load_words<KPAD>(wf, a.k_words + ((int64_t)head * N + T * BN + t) * w64, w64, t < prm.fold);
             load_words<KPAD>(wq0, a.q_words + ((int64_t)head * N + row0 + t) * w64, w64, row0 + t < N);
             load_words<KPAD>(wq1, a.q_words + ((int64_t)head * N + row0 + t + 64) * w64, w64, row0 + t + 64 < N);
             load_words<KPAD>(wk, a.k_words + ((int64_t)head * N + t) * w64, w64, t < N);
@@ -825,9 +834,27 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             fence_proxy_async();
             warp_arrive(&sm->qfull[qr.stage], lane);
             qr.next(prm.qst);
-            // Q words of the next unit: their latency hides behind this unit's K tiles
             const int un = u + G;
             const int hn = un / prm.mblocks;
+            if constexpr (FOLD) {
+                // the folded keys' packed words go to the softmax threads through shared memory (they used to prefetch
+                // them from global memory into 16 registers each, which cost the tile loop a spill)
+                if (warp == 6) {
+                    mbar_wait(&sm->ffree[fr.stage], fr.phase ^ 1u);
+                    if (t < kFoldMax) {
+#pragma unroll
+                        for (int w = 0; w < 2; ++w) {
+                            const uint32_t lo = 2 * w < KPAD / 32 ? wf[(2 * w) % (KPAD / 32)] : 0u;
+                            const uint32_t hi = 2 * w + 1 < KPAD / 32 ? wf[(2 * w + 1) % (KPAD / 32)] : 0u;
+                            sm->kbits[fr.stage][t][w] = ((uint64_t)hi << 32) | lo;
+                        }
+                    }
+                    warp_arrive(&sm->ffull[fr.stage], lane);
+                    fr.next(2);
+                    if (un < prm.units) load_words<KPAD>(wf, a.k_words + ((int64_t)hn * N + T * BN + t) * w64, w64, t < prm.fold);
+                }
+            }
+            // Q words of the next unit: their latency hides behind this unit's K tiles
             if (un < prm.units) {
                 const int rn = (un - hn * prm.mblocks) * BM;
                 load_words<KPAD>(wq0, a.q_words + ((int64_t)hn * N + rn + t) * w64, w64, rn + t < N);
@@ -878,7 +905,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MODE == 1 ? kRegsSoftmax : kRegsSoftmax - 8));
         // ============================================================ softmax + epilogue (thread = query row)
         const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-        Ring br;
+        Ring br, fr;
         uint32_t g = 0;  // tiles consumed so far (S stage = g & 1)
         // per-head scales are fetched one unit ahead and only combined when used (an early multiply would stall this
         // in-order thread on the global loads)
@@ -943,19 +970,14 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             // requested now and only turned into logits at the unit's last tile, so the loads cost no wait
             constexpr int W = (KPAD + 63) / 64;
             constexpr int NF = FOLD ? kFoldMax : 1;
-            uint64_t fq[W], fk[NF][W];
+            uint64_t fq[W];
             float fb[NF];                       // BIAS 2: values; BIAS 1: unused (the raw 16-byte vector fbraw is unpacked at use --
             uint4 fbraw = make_uint4(0, 0, 0, 0);  // converting here would stall this in-order thread on the load)
             if (FOLD && warp_ok) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) fq[w] = (row_ok && w < w64) ? __ldg(a.q_words + (uint32_t)((head * N + row) * w64 + w)) : 0ull;
 #pragma unroll
-                for (int i = 0; i < NF; ++i) {
-#pragma unroll
-                    for (int w = 0; w < W; ++w)
-                        fk[i][w] = (i < prm.fold && w < w64) ? __ldg(a.k_words + (uint32_t)((head * N + T * BN + i) * w64 + w)) : 0ull;
-                    fb[i] = 0.f;
-                }
+                for (int i = 0; i < NF; ++i) fb[i] = 0.f;
                 if ((BIAS == 1 || BIAS == 2) && row_ok) {
                     const char* brow_g = static_cast<const char*>(a.bias) + ((int64_t)bias_tab * N + row) * a.bias_ld * dtype_size(a.bias_dtype);
                     if (BIAS == 1) {  // bf16 rows padded to 16 bytes: the 8 columns after the last full tile are one vector
@@ -985,6 +1007,11 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         warp_arrive(&sm->bfree[br.stage], lane);
                         br.next(prm.bst);
                     }
+                    if (FOLD && j == T - 1) {
+                        mbar_wait(&sm->ffull[fr.stage], fr.phase);
+                        warp_arrive(&sm->ffree[fr.stage], lane);
+                        fr.next(2);
+                    }
                     tc_fence_before();
                     warp_arrive(&sm->pfull[s], lane);
                 } else {
@@ -1008,10 +1035,13 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                         // compiler would otherwise hoist them to the unit header and stall there on the loads
 #pragma unroll
                         for (int w = 0; w < W; ++w) asm volatile("" : "+l"(fq[w]));
+                        // the keys' words were staged by the expander warp (zeros past prm.fold and past w64)
+                        uint64_t fk[NF][W];
+                        mbar_wait(&sm->ffull[fr.stage], fr.phase);
 #pragma unroll
                         for (int i = 0; i < NF; ++i)
 #pragma unroll
-                            for (int w = 0; w < W; ++w) asm volatile("" : "+l"(fk[i][w]));
+                            for (int w = 0; w < W; ++w) fk[i][w] = sm->kbits[fr.stage][i][w];
                         asm volatile("" : "+r"(fbraw.x), "+r"(fbraw.y), "+r"(fbraw.z), "+r"(fbraw.w));
                         if (BIAS == 1) {
                             const uint32_t bw[4] = {fbraw.x, fbraw.y, fbraw.z, fbraw.w};
@@ -1034,6 +1064,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                                 if (DBG && dbg_row) dbg_row[BN + i] = d - 2 * pc;
                             }
                         }
+                        warp_arrive(&sm->ffree[fr.stage], lane);
+                        fr.next(2);
                     }
                     if (MODE != 0 || nk == BN)
                         softmax_tile<BIAS, ROWSUM, true, DBG, TL>(tl_buf, tl_n, sm, rs, x, s_addr, lane_base, brow, br.stage, bias_row,
@@ -1132,7 +1164,8 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
         configured[dev] = true;
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
-    const int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
+    int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
+    if (env_long("BA_GRID", 0) > 0) grid = (int)std::min<long>(prm.units, env_long("BA_GRID", 0));  // dev knob
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
