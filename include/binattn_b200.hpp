@@ -105,6 +105,11 @@ inline std::uint16_t to_bf16_bits(double x) {  // round-to-nearest-even
     return static_cast<std::uint16_t>(u >> 16);
 }
 
+struct FidelityReport {  // fidelity.hpp:12-18
+    double cos_sim = 0.0, relative_l1 = 0.0, rmse = 0.0, precision_at_k = 0.0;
+    std::size_t k = 0;
+};
+
 // One ba_handle per device; not copyable.
 class Engine {
 public:
@@ -184,6 +189,18 @@ public:
         cfg.bias = bias;
         cfg.precision = precision;
         return binary_attention_fused(q, k, v, cfg).output;
+    }
+
+    // binattn::attention_fidelity(p_ref, p_other, k) (fidelity.hpp:40-41): same checks, same exception types.
+    template <class DenseMatrixT>
+    FidelityReport attention_fidelity(const DenseMatrixT& p_ref, const DenseMatrixT& p_other, std::size_t k) const {
+        if (p_ref.rows() != p_other.rows() || p_ref.cols() != p_other.cols())
+            throw ShapeError("attention_fidelity: shape mismatch");  // fidelity.cpp:42-43
+        if (k == 0) throw ValidationError("attention_fidelity: k must be >= 1");  // fidelity.cpp:44
+        ba_fidelity f{};
+        check(ba_attention_fidelity_host(h_, p_ref.data().data(), p_other.data().data(), static_cast<int64_t>(p_ref.rows()),
+                                         static_cast<int64_t>(p_ref.cols()), static_cast<int64_t>(k), &f));
+        return FidelityReport{f.cos_sim, f.relative_l1, f.rmse, f.precision_at_k, k};
     }
 
 private:

@@ -99,6 +99,28 @@ int ba_quantize_values(ba_handle* h, const ba_params* p, const void* V, int8_t* 
 int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, const uint64_t* k_words,
                      int64_t head_index, int32_t* S, void* stream);
 
+/* Attention-map rows of ONE head for the fidelity diagnostics (the reference's `with_probs` outputs):
+ *   P[r, :] = softmax_j(score(rows[r], j)), fp64 [nrows, N] (device), rows = device int32 [nrows] query-row indices.
+ *   mode BA_PROBS_FULL    score = q_i.k_j / tau + bias                        reference_attention      (attention.cpp:99-147)
+ *   mode BA_PROBS_BINARY  score = mu_q*mu_k*(d - 2 popc(q^k)) / tau + bias    binary_attention_unfused (attention.cpp:149-248)
+ * Q, K: [B,H,N,d] in_dtype; bias as in ba_binary_attention_fwd.  mu and the sign bits are computed in the call (fp64). */
+enum { BA_PROBS_FULL = 0, BA_PROBS_BINARY = 1 };
+int ba_attention_probs(ba_handle* h, const ba_params* p, int mode, const void* Q, const void* K, const void* bias,
+                       int64_t head_index, const int32_t* rows, int nrows, double* P, void* stream);
+
+/* attention_fidelity (fidelity.hpp:12-18, fidelity.cpp:40-85) of two row-stochastic fp64 [rows, cols] device matrices:
+ * flattened cosine, ||ref-other||_1 / ||ref||_1, RMSE, mean per-row top-k overlap / k' (k' = min(k, cols), ties toward the
+ * lower column).  Rows must be probability vectors to 1e-6 (BA_ERR_VALIDATION otherwise, fidelity.cpp:12-24), k >= 1.
+ * Synchronises `stream`; the result is written to host memory. */
+typedef struct ba_fidelity {
+    double cos_sim, relative_l1, rmse, precision_at_k;
+} ba_fidelity;
+int ba_attention_fidelity(ba_handle* h, const double* p_ref, const double* p_other, int64_t rows, int64_t cols, int64_t k,
+                          ba_fidelity* out, void* stream);
+/* Same with HOST matrices (what a reference caller holds: DenseMatrix::data()); staged through device memory. */
+int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* p_other, int64_t rows, int64_t cols, int64_t k,
+                               ba_fidelity* out);
+
 /* binary_attention_fused (attention.cpp:250-382), quantize_pv = false semantics, for all B*H heads.
  * row_max / row_sum: optional [B,H,N] float32 (AttentionOutput::row_max / row_sum, attention.hpp:45-46).
  * quantize_pv = 1 selects the reference's integer P.V mode (attention.cpp:332-343, 361-363). */

@@ -253,6 +253,78 @@ static int bo_check_cfg(size_t n, size_t d, double tau, size_t br, size_t bc) {
     return BO_OK;
 }
 
+/* fidelity.cpp:12-24 check_row_stochastic: weights >= -1e-6, every row sums to 1 within 1e-6 */
+static int bo_check_row_stochastic(const double *p, size_t rows, size_t cols) {
+    for (size_t i = 0; i < rows; ++i) {
+        double sum = 0.0;
+        for (size_t j = 0; j < cols; ++j) {
+            const double v = p[i * cols + j];
+            if (v < -1e-6) return BO_EVALID;
+            sum += v;
+        }
+        if (fabs(sum - 1.0) > 1e-6) return BO_EVALID;
+    }
+    return BO_OK;
+}
+
+/* fidelity.cpp:26-36 topk_indices: the k largest entries, ties broken toward the lower index (selection form) */
+static void bo_topk(const double *row, size_t n, size_t k, char *used, size_t *out) {
+    memset(used, 0, n);
+    for (size_t t = 0; t < k; ++t) {
+        size_t best = n;
+        for (size_t j = 0; j < n; ++j) {
+            if (used[j]) continue;
+            if (best == n || row[j] > row[best]) best = j;
+        }
+        used[best] = 1;
+        out[t] = best;
+    }
+}
+
+/* fidelity.cpp:40-85 attention_fidelity: out = {cos_sim, relative_l1, rmse, precision_at_k} */
+int bo_attention_fidelity(const double *p_ref, const double *p_other, size_t rows, size_t cols, size_t k, double *out) {
+    if (rows == 0 || cols == 0) return BO_ESHAPE;
+    if (k == 0) return BO_EVALID;
+    int rc = bo_check_row_stochastic(p_ref, rows, cols);
+    if (rc) return rc;
+    rc = bo_check_row_stochastic(p_other, rows, cols);
+    if (rc) return rc;
+    const size_t count = rows * cols;
+    double dot = 0.0, na = 0.0, nb = 0.0, l1_diff = 0.0, l1_ref = 0.0, sq = 0.0;
+    for (size_t t = 0; t < count; ++t) {
+        const double a = p_ref[t], b = p_other[t];
+        dot += a * b;
+        na += a * a;
+        nb += b * b;
+        l1_diff += fabs(a - b);
+        l1_ref += fabs(a);
+        sq += (a - b) * (a - b);
+    }
+    out[0] = dot / (sqrt(na) * sqrt(nb));
+    out[1] = l1_diff / l1_ref;
+    out[2] = sqrt(sq / (double)count);
+    const size_t keff = k < cols ? k : cols;
+    char *used = (char *)malloc(cols), *in_a = (char *)malloc(cols);
+    size_t *ta = (size_t *)malloc(keff * sizeof(size_t)), *tb = (size_t *)malloc(keff * sizeof(size_t));
+    if (!used || !in_a || !ta || !tb) {
+        free(used); free(in_a); free(ta); free(tb);
+        return BO_ENOMEM;
+    }
+    double prec = 0.0;
+    for (size_t i = 0; i < rows; ++i) {
+        bo_topk(p_ref + i * cols, cols, keff, used, ta);
+        bo_topk(p_other + i * cols, cols, keff, used, tb);
+        memset(in_a, 0, cols);
+        for (size_t t = 0; t < keff; ++t) in_a[ta[t]] = 1;
+        size_t hits = 0;
+        for (size_t t = 0; t < keff; ++t) hits += (size_t)in_a[tb[t]];
+        prec += (double)hits / (double)keff;
+    }
+    out[3] = prec / (double)rows;
+    free(used); free(in_a); free(ta); free(tb);
+    return BO_OK;
+}
+
 /* attention.cpp:99-147 reference_attention (fp64 dense softmax attention) */
 int bo_reference_attention(const double *q, const double *k, const double *v, size_t n, size_t d, double tau,
                            const double *bias /* n*n or NULL */, double *y, double *m, double *l,

@@ -62,6 +62,7 @@ class CpuLib:
         getattr(L, p + "reference_attention").argtypes = [_f64, _f64, _f64, sz, sz, C.c_double, vp, _f64, _f64, _f64, vp]
         getattr(L, p + "binary_attention_unfused").argtypes = [_f64, _f64, _f64, sz, sz, C.c_double, C.c_int, vp, _f64, _f64, _f64, vp]
         getattr(L, p + "binary_attention_fused").argtypes = [_f64, _f64, _f64, sz, sz, C.c_double, sz, sz, C.c_int, vp, _f64, _f64, _f64]
+        getattr(L, p + "attention_fidelity").argtypes = [_f64, _f64, sz, sz, sz, _f64]
         if self.is_reference:
             L.ref_materialize_bias_rel2d.argtypes = [_f64, _f64, sz, sz, _f64]
             L.ref_rng_new.restype = vp
@@ -196,6 +197,16 @@ class CpuLib:
         y, m, l = np.zeros((n, d)), np.zeros(n), np.zeros(n)
         self._chk(self._f("binary_attention_fused")(q, k, v, n, d, tau, br, bc, int(quantize_pv), _opt(bias), y, m, l))
         return y, m, l
+
+    def attention_fidelity(self, p_ref, p_other, k: int):
+        """fidelity.cpp:40-85 -> (cos_sim, relative_l1, rmse, precision_at_k)."""
+        p_ref = np.ascontiguousarray(p_ref, dtype=np.float64)
+        p_other = np.ascontiguousarray(p_other, dtype=np.float64)
+        if p_ref.ndim != 2 or p_ref.shape != p_other.shape:
+            raise CpuError(1)  # fidelity.cpp:42-43 ShapeError
+        out = np.zeros(4)
+        self._chk(self._f("attention_fidelity")(p_ref, p_other, p_ref.shape[0], p_ref.shape[1], k, out))
+        return tuple(float(x) for x in out)
 
     def binary_attention_fused_heads(self, q, k, v, tau=None, bias=None, quantize_pv=False, nthreads=1, intra_threads=1):
         """q,k,v: [heads, n, d] float64; bias: [bias_heads, n, n] or None.  Heads spread over host threads."""

@@ -17,6 +17,7 @@
 #include "binattn/errors.hpp"
 #include "binattn/tensor_file.hpp"
 #include "binattn/bitops.hpp"
+#include "binattn/fidelity.hpp"
 #include "binattn/parallel.hpp"
 #include "binattn/quantize.hpp"
 #include "binattn/rng.hpp"
@@ -141,6 +142,18 @@ int ref_materialize_bias_rel2d(const double* row_off, const double* col_off, std
                                     std::vector<double>(col_off, col_off + g2m1)}},
             n);
         std::memcpy(table, b.data().data(), n * n * sizeof(double));
+    });
+}
+
+// fidelity.cpp:40-85 attention_fidelity -> {cos_sim, relative_l1, rmse, precision_at_k}
+int ref_attention_fidelity(const double* p_ref, const double* p_other, std::size_t rows, std::size_t cols, std::size_t k,
+                           double* out) {
+    return guarded([&] {
+        const FidelityReport r = attention_fidelity(dm(p_ref, rows, cols), dm(p_other, rows, cols), k);
+        out[0] = r.cos_sim;
+        out[1] = r.relative_l1;
+        out[2] = r.rmse;
+        out[3] = r.precision_at_k;
     });
 }
 

@@ -58,6 +58,20 @@ class _Params(C.Structure):
 _lib = None
 
 
+class _Fidelity(C.Structure):  # ba_fidelity (include/binattn_cuda.h)
+    _fields_ = [("cos_sim", C.c_double), ("relative_l1", C.c_double), ("rmse", C.c_double), ("precision_at_k", C.c_double)]
+
+
+@dataclass
+class FidelityReport:
+    """binattn::FidelityReport (fidelity.hpp:12-18)."""
+    cos_sim: float
+    relative_l1: float
+    rmse: float
+    precision_at_k: float
+    k: int
+
+
 def load_library() -> C.CDLL:
     """Load libbinattn_cuda.so (built in-tree by paper_2603_09582_b200/build.py).  Fails loudly if absent."""
     global _lib
@@ -76,6 +90,8 @@ def load_library() -> C.CDLL:
     lib.ba_binary_logits.argtypes = [vp, C.POINTER(_Params), vp, vp, i64, vp, vp]
     lib.ba_quantize_values.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp]
     lib.ba_binary_attention_fwd.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.ba_attention_probs.argtypes = [vp, C.POINTER(_Params), C.c_int, vp, vp, vp, i64, vp, C.c_int, vp, vp]
+    lib.ba_attention_fidelity.argtypes = [vp, vp, vp, i64, i64, i64, C.POINTER(_Fidelity), vp]
     lib.ba_binary_attention_host.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]
     lib.ba_shard_range.argtypes = [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
     lib.ba_select_kernel.argtypes = [C.POINTER(_Params)]
@@ -278,6 +294,35 @@ class BinaryAttention:
         _check(self.lib.ba_binary_logits(self.h, C.byref(p), _ptr(q_words.contiguous()), _ptr(k_words.contiguous()),
                                          head, _ptr(S), self._stream()))
         return S
+
+    def attention_probs(self, Q, K, bias=None, scale=None, head: int = 0, rows=None, binary: bool = True) -> torch.Tensor:
+        """Attention-map rows of one head, float64 [len(rows), N] (the reference's `with_probs` output restricted to
+        sampled query rows): binary=True follows binary_attention_unfused (attention.cpp:149-248), binary=False the
+        full-precision reference_attention (attention.cpp:99-147).  `head` indexes the flattened [B*H] grid."""
+        if Q.dim() != 4 or K.shape != Q.shape:
+            raise ShapeError("attention: Q, K must be [B,H,N,d]")
+        B, H, N, d = Q.shape
+        Q, K = Q.contiguous(), K.contiguous()
+        bias, bias_t = self._check_bias(bias, H, N)
+        p = self._params(B, H, N, d, Q.dtype, bias, scale)
+        rows_t = torch.arange(N, device=Q.device, dtype=torch.int32) if rows is None else \
+            torch.as_tensor(rows, dtype=torch.int32).to(Q.device).contiguous()
+        if rows_t.numel() < 1 or int(rows_t.min()) < 0 or int(rows_t.max()) >= N:
+            raise ShapeError("attention_probs: rows must be a non-empty list of indices in [0, N)")
+        P = torch.empty((rows_t.numel(), N), dtype=torch.float64, device=Q.device)
+        _check(self.lib.ba_attention_probs(self.h, C.byref(p), 1 if binary else 0, _ptr(Q), _ptr(K), _ptr(bias_t), head,
+                                           _ptr(rows_t), rows_t.numel(), _ptr(P), self._stream()))
+        return P
+
+    def attention_fidelity(self, p_ref: torch.Tensor, p_other: torch.Tensor, k: int) -> "FidelityReport":
+        """attention_fidelity (fidelity.cpp:40-85) of two row-stochastic [rows, cols] device matrices."""
+        if p_ref.dim() != 2 or p_ref.shape != p_other.shape:
+            raise ShapeError("attention_fidelity: shape mismatch")  # fidelity.cpp:42-43
+        a = p_ref.to(torch.float64).contiguous()
+        b = p_other.to(torch.float64).contiguous()
+        out = _Fidelity()
+        _check(self.lib.ba_attention_fidelity(self.h, _ptr(a), _ptr(b), a.shape[0], a.shape[1], int(k), C.byref(out), self._stream()))
+        return FidelityReport(out.cos_sim, out.relative_l1, out.rmse, out.precision_at_k, int(k))
 
     def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False, quantize_pv=False, block_cols=None):
         """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output).

@@ -45,6 +45,13 @@ int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, in
                            cudaStream_t stream);
 int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream);
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
+// diagnostics (fidelity.cu)
+int launch_head_mean_abs(const void* Q, const void* K, int dtype, int64_t count, double* mu, cudaStream_t stream);
+int launch_probs_rows(const void* Q, const void* K, const void* bias, const int32_t* rows, int nrows, const double* mu, double* P,
+                      double tau, int64_t bias_ld, int N, int d, int in_dtype, int bias_dtype, int bias_kind, int mode,
+                      cudaStream_t stream);
+int fidelity_topk_max();
+int launch_fidelity_rows(const double* A, const double* B, int64_t rows, int cols, int keff, double* partial, cudaStream_t stream);
 bool tcgen05_supported(const ba_params* p, const char** why);
 
 __device__ __forceinline__ float to_float(float x) { return x; }

@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <cmath>
+#include <vector>
 
 #include "ba_common.cuh"
 
@@ -113,6 +115,8 @@ struct ba_handle {
     size_t tickets_n = 0;
     float* partials = nullptr;  // for standalone ba_pack_signs
     size_t partials_n = 0;
+    double* diag = nullptr;     // {mu_q, mu_k} of ba_attention_probs
+    size_t diag_bytes = 0;
     // host-buffer path: copy-in stream, compute stream, copy-out stream + per-chunk events
     cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
     cudaEvent_t ev_in[kHostChunksMax] = {}, ev_done[kHostChunksMax] = {};
@@ -190,6 +194,7 @@ int ba_destroy(ba_handle* h) {
     if (h->ws) cudaFree(h->ws);
     if (h->tickets) cudaFree(h->tickets);
     if (h->partials) cudaFree(h->partials);
+    if (h->diag) cudaFree(h->diag);
     for (void* s : h->stage)
         if (s) cudaFree(s);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -313,6 +318,101 @@ int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, 
     if (n < 0) return fail(BA_ERR_CUDA, "binary_logits launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
     return BA_OK;
+}
+
+int ba_attention_probs(ba_handle* h, const ba_params* p, int mode, const void* Q, const void* K, const void* bias,
+                       int64_t head_index, const int32_t* rows, int nrows, double* P, void* stream) {
+    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
+    int rc = check_params(p, true);
+    if (rc) return rc;
+    if (mode != BA_PROBS_FULL && mode != BA_PROBS_BINARY) return fail(BA_ERR_VALIDATION, "attention_probs: unknown mode %d", mode);
+    if (!Q || !K || !rows || !P) return fail(BA_ERR_SHAPE, "attention_probs: NULL pointer");
+    if (p->bias_mode != BA_BIAS_NONE && !bias) return fail(BA_ERR_SHAPE, "attention_probs: bias_mode set but bias is NULL");
+    if (nrows < 1) return fail(BA_ERR_SHAPE, "attention_probs: nrows must be >= 1");
+    const int64_t BH = (int64_t)p->B * p->H;
+    if (head_index < 0 || head_index >= BH)
+        return fail(BA_ERR_SHAPE, "attention_probs: head %lld outside [0,%lld)", (long long)head_index, (long long)BH);
+    BA_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    rc = ensure(reinterpret_cast<void**>(&h->diag), &h->diag_bytes, 2 * sizeof(double), false);
+    if (rc) return rc;
+    const int64_t head_elems = (int64_t)p->N * p->d;
+    const char* q = static_cast<const char*>(Q) + head_index * head_elems * ba::dtype_size(p->in_dtype);
+    const char* k = static_cast<const char*>(K) + head_index * head_elems * ba::dtype_size(p->in_dtype);
+    const int64_t bias_ld = p->bias_ld ? p->bias_ld : p->N;
+    const char* b = nullptr;
+    if (p->bias_mode != BA_BIAS_NONE) {
+        const int64_t tab = (head_index % p->H) % p->bias_heads;
+        const int64_t per = p->bias_mode == BA_BIAS_REL1D ? 2 * (int64_t)p->N - 1 : (int64_t)p->N * bias_ld;
+        b = static_cast<const char*>(bias) + tab * per * ba::dtype_size(p->bias_dtype);
+    }
+    int n = 0;
+    if (mode == BA_PROBS_BINARY) {
+        n = ba::launch_head_mean_abs(q, k, p->in_dtype, head_elems, h->diag, st);
+        if (n < 0) return fail(BA_ERR_CUDA, "attention_probs (mean abs) launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+        h->launches += n;
+    }
+    n = ba::launch_probs_rows(q, k, b, rows, nrows, h->diag, P, 1.0 / (double)p->inv_tau, bias_ld, p->N, p->d, p->in_dtype,
+                              p->bias_dtype, p->bias_mode, mode, st);
+    if (n < 0) return fail(BA_ERR_CUDA, "attention_probs launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+    h->launches += n;
+    return BA_OK;
+}
+
+int ba_attention_fidelity(ba_handle* h, const double* p_ref, const double* p_other, int64_t rows, int64_t cols, int64_t k,
+                          ba_fidelity* out, void* stream) {
+    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
+    if (!p_ref || !p_other || !out) return fail(BA_ERR_SHAPE, "attention_fidelity: NULL pointer");
+    if (rows < 1 || cols < 1 || cols > INT32_MAX) return fail(BA_ERR_SHAPE, "attention_fidelity: shape mismatch");  // fidelity.cpp:42-43
+    if (k < 1) return fail(BA_ERR_VALIDATION, "attention_fidelity: k must be >= 1");                                // fidelity.cpp:44
+    const int64_t keff = k < cols ? k : cols;
+    if (keff > ba::fidelity_topk_max())
+        return fail(BA_ERR_UNSUPPORTED, "attention_fidelity: min(k, cols) = %lld > %d is not supported", (long long)keff,
+                    ba::fidelity_topk_max());
+    BA_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* partial = nullptr;
+    BA_CUDA(cudaMalloc(&partial, (size_t)rows * 8 * sizeof(double)));
+    const int n = ba::launch_fidelity_rows(p_ref, p_other, rows, (int)cols, (int)keff, partial, st);
+    if (n < 0) {
+        cudaFree(partial);
+        return fail(BA_ERR_CUDA, "attention_fidelity launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+    }
+    h->launches += n;
+    std::vector<double> host((size_t)rows * 8);
+    cudaError_t e = cudaMemcpyAsync(host.data(), partial, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(partial);
+    if (e != cudaSuccess) return fail(BA_ERR_CUDA, "attention_fidelity: %s", cudaGetErrorString(e));
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t r = 0; r < rows; ++r) {  // rows added in order: deterministic
+        if (host[r * 8 + 7] != 0.0)
+            return fail(BA_ERR_VALIDATION, "attention_fidelity: row %lld is not a probability vector (1e-6)", (long long)r);
+        for (int c = 0; c < 7; ++c) acc[c] += host[r * 8 + c];
+    }
+    out->cos_sim = acc[0] / (std::sqrt(acc[1]) * std::sqrt(acc[2]));
+    out->relative_l1 = acc[3] / acc[4];
+    out->rmse = std::sqrt(acc[5] / ((double)rows * (double)cols));
+    out->precision_at_k = acc[6] / (double)rows;
+    return BA_OK;
+}
+
+int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* p_other, int64_t rows, int64_t cols, int64_t k,
+                               ba_fidelity* out) {
+    if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
+    if (!p_ref || !p_other || !out) return fail(BA_ERR_SHAPE, "attention_fidelity: NULL pointer");
+    if (rows < 1 || cols < 1) return fail(BA_ERR_SHAPE, "attention_fidelity: shape mismatch");
+    BA_CUDA(cudaSetDevice(h->device));
+    const size_t bytes = (size_t)rows * (size_t)cols * sizeof(double);
+    double* dev = nullptr;
+    BA_CUDA(cudaMalloc(&dev, 2 * bytes));
+    cudaError_t e = cudaMemcpy(dev, p_ref, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dev + (size_t)rows * cols, p_other, bytes, cudaMemcpyHostToDevice);
+    int rc = BA_OK;
+    if (e != cudaSuccess) rc = fail(BA_ERR_CUDA, "attention_fidelity: %s", cudaGetErrorString(e));
+    else rc = ba_attention_fidelity(h, dev, dev + (size_t)rows * cols, rows, cols, k, out, nullptr);
+    cudaFree(dev);
+    return rc;
 }
 
 // One K1 + K2 pass over `heads` consecutive heads starting at grid index head0; every tensor pointer already points at

@@ -14,5 +14,8 @@ ba.forward(Q.float(), K.float(), V.float(), bias.float(), kernel="simt")
 ba.forward(Q, K, V, bias, quantize_pv=True)
 ba.forward(Q, K, V, pkg.Relative1dBias(torch.randn(H, 2 * N - 1, device="cuda")), kernel="simt")
 ba.quantize_values(V)
+Pb = ba.attention_probs(Q, K, bias, head=1, rows=[0, 7, 149])
+Pf = ba.attention_probs(Q, K, bias, head=1, rows=[0, 7, 149], binary=False)
+ba.attention_fidelity(Pf, Pb, 5)
 torch.cuda.synchronize()
 print("ok")

@@ -16,6 +16,11 @@ void bo_rng_init(void* r, uint64_t seed, uint64_t stream);
 void bo_random_dense(void* r, size_t count, double scale, double* out);
 int bo_binary_attention_fused(const double* q, const double* k, const double* v, size_t n, size_t d, double tau,
                               size_t br, size_t bc, int qpv, const double* bias, double* y, double* m, double* l);
+int bo_reference_attention(const double* q, const double* k, const double* v, size_t n, size_t d, double tau,
+                           const double* bias, double* y, double* m, double* l, double* probs);
+int bo_binary_attention_unfused(const double* q, const double* k, const double* v, size_t n, size_t d, double tau, int qpv,
+                                const double* bias, double* y, double* m, double* l, double* probs);
+int bo_attention_fidelity(const double* p_ref, const double* p_other, size_t rows, size_t cols, size_t k, double* out);
 }
 
 struct Span {
@@ -179,6 +184,35 @@ int main() {
             bad.rel1d_offsets.pop_back();
             CHECK(throws<ShapeError>([&] { eng.binary_attention_fused(q, k, v, bad); }));  // attention.cpp:66-67
         }
+    }
+    {  // attention_fidelity (fidelity.cpp:40-85): the full-precision attention map against the binary one, and the KATs of
+       // test_fidelity.cpp:80-87 (ties go to the lower column) and :163-170 (validation)
+        const std::size_t n = 96, d = 32;
+        bo_rng_init(rng.data(), 52, 0);
+        const Mat q = rounded(random_dense(rng.data(), n, d), Precision::bf16), k = rounded(random_dense(rng.data(), n, d), Precision::bf16),
+                  v = rounded(random_dense(rng.data(), n, d), Precision::bf16);
+        std::vector<double> y(n * d), m(n), l(n), pf(n * n), pb(n * n), want(4);
+        CHECK(bo_reference_attention(q.data().data(), k.data().data(), v.data().data(), n, d, std::sqrt((double)d), nullptr, y.data(),
+                                     m.data(), l.data(), pf.data()) == 0);
+        CHECK(bo_binary_attention_unfused(q.data().data(), k.data().data(), v.data().data(), n, d, std::sqrt((double)d), 0, nullptr,
+                                          y.data(), m.data(), l.data(), pb.data()) == 0);
+        const Mat p_full(n, n, pf), p_bin(n, n, pb);
+        for (std::size_t kk : {std::size_t{1}, std::size_t{5}, std::size_t{500}}) {
+            CHECK(bo_attention_fidelity(pf.data(), pb.data(), n, n, kk, want.data()) == 0);
+            const FidelityReport r = eng.attention_fidelity(p_full, p_bin, kk);
+            std::printf("attention_fidelity k=%zu  cos=%.6f rel_l1=%.6f rmse=%.3e prec@k=%.4f\n", kk, r.cos_sim, r.relative_l1, r.rmse,
+                        r.precision_at_k);
+            CHECK(r.precision_at_k == want[3] && r.k == kk);
+            CHECK(std::fabs(r.cos_sim - want[0]) <= 1e-12 && std::fabs(r.relative_l1 - want[1]) <= 1e-12 * want[1] &&
+                  std::fabs(r.rmse - want[2]) <= 1e-12 * want[2]);
+        }
+        std::vector<double> uni(16, 0.25), hot0(16, 0.0), hot2(16, 0.0), half(16, 0.5);
+        for (int i = 0; i < 4; ++i) hot0[i * 4] = 1.0, hot2[i * 4 + 2] = 1.0;
+        CHECK(eng.attention_fidelity(Mat(4, 4, hot0), Mat(4, 4, uni), 1).precision_at_k == 1.0);
+        CHECK(eng.attention_fidelity(Mat(4, 4, hot2), Mat(4, 4, uni), 1).precision_at_k == 0.0);
+        CHECK(throws<ShapeError>([&] { eng.attention_fidelity(Mat(4, 4, uni), Mat(2, 8, uni), 2); }));
+        CHECK(throws<ValidationError>([&] { eng.attention_fidelity(Mat(4, 4, uni), Mat(4, 4, half), 2); }));
+        CHECK(throws<ValidationError>([&] { eng.attention_fidelity(Mat(4, 4, uni), Mat(4, 4, uni), 0); }));
     }
     std::printf(failures ? "FAILED (%d)\n" : "ALL OK\n", failures);
     return failures ? 1 : 0;

@@ -280,3 +280,90 @@ def test_heads_driver_matches_single_calls(port):
     y = port.binary_attention_fused_heads(q, k, v, bias=bias, nthreads=2)
     for h in range(3):
         assert np.array_equal(y[h], port.binary_attention_fused(q[h], k[h], v[h], bias=bias[h % 2])[0])
+
+
+# ---------------------------------------------------------------- attention-map fidelity KATs (test_fidelity.cpp)
+def _row_stochastic(rng, n, cols):
+    p = rng.random((n, cols))
+    return p / p.sum(axis=1, keepdims=True)
+
+
+def _brute_precision(a, b, k):  # test_fidelity.cpp:28-57 (selection with lower-index tie-breaks)
+    n, cols = a.shape
+    keff = min(k, cols)
+
+    def topk(row):
+        used, picked = set(), []
+        for _ in range(keff):
+            best = None
+            for j in range(cols):
+                if j in used:
+                    continue
+                if best is None or row[j] > row[best]:
+                    best = j
+            used.add(best)
+            picked.append(best)
+        return picked
+    return sum(len(set(topk(a[i])) & set(topk(b[i]))) / keff for i in range(n)) / n
+
+
+def test_fidelity_self_comparison(port):  # test_fidelity.cpp:70-78
+    p = _row_stochastic(np.random.default_rng(61), 6, 6)
+    cos, rl1, rmse, prec = port.attention_fidelity(p, p, 3)
+    assert abs(cos - 1.0) <= 4e-16 and (rl1, rmse, prec) == (0.0, 0.0, 1.0)  # (sqrt(x)*sqrt(x) may round off x by an ulp)
+
+
+def test_fidelity_tie_break_toward_lower_index(port):  # test_fidelity.cpp:80-87
+    n = 4
+    uni = np.full((n, n), 1.0 / n)
+    hot0, hot2 = np.zeros((n, n)), np.zeros((n, n))
+    hot0[:, 0] = 1.0
+    hot2[:, 2] = 1.0
+    assert port.attention_fidelity(hot0, uni, 1)[3] == 1.0
+    assert port.attention_fidelity(hot2, uni, 1)[3] == 0.0
+
+
+def test_fidelity_matches_brute_force(port):  # test_fidelity.cpp:89-109
+    rng = np.random.default_rng(62)
+    a, b = _row_stochastic(rng, 8, 8), _row_stochastic(rng, 8, 8)
+    cos, rl1, rmse, prec = port.attention_fidelity(a, b, 3)
+    assert prec == _brute_precision(a, b, 3)
+    assert cos == pytest.approx((a * b).sum() / np.sqrt((a * a).sum() * (b * b).sum()), rel=1e-12)
+    assert rl1 == pytest.approx(np.abs(a - b).sum() / np.abs(a).sum(), rel=1e-12)
+    assert rmse == pytest.approx(np.sqrt(((a - b) ** 2).mean()), rel=1e-12)
+
+
+def test_fidelity_k_clamps_and_asymmetry(port):  # test_fidelity.cpp:111-135
+    rng = np.random.default_rng(63)
+    a, b = _row_stochastic(rng, 4, 4), _row_stochastic(rng, 4, 4)
+    assert port.attention_fidelity(a, b, 100)[3] == 1.0
+    a, b = _row_stochastic(rng, 5, 7), _row_stochastic(rng, 5, 7)
+    ab, ba_ = port.attention_fidelity(a, b, 2), port.attention_fidelity(b, a, 2)
+    assert ab[2] == ba_[2]
+    assert ab[1] == pytest.approx(np.abs(a - b).sum() / np.abs(a).sum(), rel=1e-12)
+    assert ba_[1] == pytest.approx(np.abs(a - b).sum() / np.abs(b).sum(), rel=1e-12)
+
+
+def test_fidelity_validation(port):  # test_fidelity.cpp:163-170
+    a = _row_stochastic(np.random.default_rng(66), 4, 4)
+    with pytest.raises(cpu.CpuError):
+        port.attention_fidelity(a, _row_stochastic(np.random.default_rng(1), 5, 5), 2)  # ShapeError
+    with pytest.raises(cpu.CpuError):
+        port.attention_fidelity(a, np.full((4, 4), 0.5), 2)  # rows sum to 2: ValidationError
+    with pytest.raises(cpu.CpuError):
+        port.attention_fidelity(a, a, 0)  # k = 0
+
+
+def test_fidelity_port_equals_reference(port, ref):
+    """Live diff against the compiled reference, on the attention maps the metric is meant for: the full-precision map
+    against the binary one (fidelity.cpp:40-85 over attention.cpp:99-147 / 149-248 with_probs)."""
+    rng = np.random.default_rng(5)
+    for n, d, k in [(33, 16, 5), (64, 32, 8), (12, 8, 20)]:
+        q, kk, v = (cpu.bf16_round(rng.standard_normal((n, d))) for _ in range(3))
+        bias = cpu.bf16_round(0.5 * rng.standard_normal((n, n)))
+        p_ref = ref.reference_attention(q, kk, v, bias=bias, with_probs=True)[3]
+        p_bin = ref.binary_attention_unfused(q, kk, v, bias=bias, with_probs=True)[3]
+        assert np.array_equal(p_bin, port.binary_attention_unfused(q, kk, v, bias=bias, with_probs=True)[3])
+        r_ref, r_port = ref.attention_fidelity(p_ref, p_bin, k), port.attention_fidelity(p_ref, p_bin, k)
+        assert r_ref[3] == r_port[3]
+        assert np.allclose(r_ref[:3], r_port[:3], rtol=1e-13, atol=0)
