@@ -15,7 +15,7 @@
 
 namespace ba {
 
-constexpr int kPackThreads = 256;
+constexpr int kPackThreads = 128;  // (256 was 11% slower at N=197: the per-thread prologue / block-sum cost is amortised over twice the vectors)
 constexpr int kPackRowsPerCta = 256;
 constexpr int kPackUnroll = 8;
 
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
     const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * 2 + (rbase * vpr + vs) * 16;
     unsigned char* wbytes = reinterpret_cast<unsigned char*>(job.words + ((int64_t)head * N + row0) * W64) + rbase * VPRP + vs;
     const int row_bytes = ROWS_PER_PASS * vpr * 16;      // byte stride between a lane's vectors of consecutive passes
-    constexpr int PASSES = kPackRowsPerCta / ROWS_PER_PASS;  // 8 (VPRP 8) or 16 (VPRP 16)
+    constexpr int PASSES = kPackRowsPerCta / ROWS_PER_PASS;  // 16 (VPRP 8) or 32 (VPRP 16)
     float s0 = 0.f, s1 = 0.f;
 #pragma unroll
     for (int p0 = 0; p0 < PASSES; p0 += kPackUnroll) {
@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
             v[u] = ldg_nc_16_pred(xbase + (p0 + u) * row_bytes, lane_act && (p0 + u) * ROWS_PER_PASS + rbase < rows);
 #pragma unroll
         for (int u = 0; u < kPackUnroll; ++u) {
+            if ((p0 + u) * ROWS_PER_PASS >= rows) break;  // block-uniform: passes past the last row do no work
             const uint32_t r[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
             uint32_t neg[4];
 #pragma unroll
