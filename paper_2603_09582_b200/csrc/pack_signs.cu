@@ -17,7 +17,7 @@ namespace ba {
 
 constexpr int kPackThreads = 128;  // (256 was 11% slower at N=197: the per-thread prologue / block-sum cost is amortised over twice the vectors)
 constexpr int kPackRowsPerCta = 256;
-constexpr int kPackUnroll = 8;
+constexpr int kPackUnroll = 16;
 
 struct PackJob {
     const void* X;
@@ -256,8 +256,13 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
     const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * 2 + (rbase * vpr + vs) * 16;
     unsigned char* wbytes = reinterpret_cast<unsigned char*>(job.words + ((int64_t)head * N + row0) * W64) + rbase * VPRP + vs;
     const int row_bytes = ROWS_PER_PASS * vpr * 16;      // byte stride between a lane's vectors of consecutive passes
-    constexpr int PASSES = kPackRowsPerCta / ROWS_PER_PASS;  // 16 (VPRP 8) or 32 (VPRP 16)
-    float s0 = 0.f, s1 = 0.f;
+    constexpr int PASSES = kPackRowsPerCta / ROWS_PER_PASS;  // 16 (VPRP 8) or 32 (VPRP 16); kPackUnroll of them are in flight at once
+    // |x| is summed by the tensor core: the four words of magnitudes are the A fragment of an m16n8k16 bf16 MMA against a
+    // B of ones, fp32 accumulate.  Which matrix position a value lands in does not matter -- every column of D holds the
+    // row sums, so the sum of all D entries is 8x the sum of all inputs -- and one HMMA replaces 8 FADD + 8 unpack ops
+    // per 16-byte vector in a kernel that is bound by instruction issue.  (bf16 x 1.0 products are exact; the fp32
+    // accumulation is deterministic on a given GPU.)
+    float dacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int p0 = 0; p0 < PASSES; p0 += kPackUnroll) {
         if (p0 * ROWS_PER_PASS >= rows) break;           // block-uniform
@@ -269,14 +274,16 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
         for (int u = 0; u < kPackUnroll; ++u) {
             if ((p0 + u) * ROWS_PER_PASS >= rows) break;  // block-uniform: passes past the last row do no work
             const uint32_t r[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-            uint32_t neg[4];
+            uint32_t neg[4], mag[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const uint32_t mag = r[i] & 0x7FFF7FFFu;
-                neg[i] = r[i] & (mag + 0x7FFF7FFFu) & 0x80008000u;  // negative and non-zero (see bf16x8_signs_abs)
-                s0 += __uint_as_float(mag << 16);
-                s1 += __uint_as_float(mag & 0xFFFF0000u);
+                mag[i] = r[i] & 0x7FFF7FFFu;
+                neg[i] = r[i] & (mag[i] + 0x7FFF7FFFu) & 0x80008000u;  // negative and non-zero (see bf16x8_signs_abs)
             }
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%8}, {%0,%1,%2,%3};"
+                : "+f"(dacc[0]), "+f"(dacc[1]), "+f"(dacc[2]), "+f"(dacc[3])
+                : "r"(mag[0]), "r"(mag[1]), "r"(mag[2]), "r"(mag[3]), "r"(0x3F803F80u));
             const uint32_t lo = __byte_perm(neg[0], neg[1], 0x7531), hi = __byte_perm(neg[2], neg[3], 0x7531);
             const uint32_t nbits = (((lo >> 7) * 0x01020408u) >> 24) | ((((hi >> 7) * 0x01020408u) >> 24) << 4);
             // every lane slot owns one BYTE of the packed row (bits 8*vs .. 8*vs+7 of the little-endian u64 words): a warp
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
             if (in_rows) wbytes[(p0 + u) * ROWS_PER_PASS * VPRP] = lane_act ? (unsigned char)(~nbits & 0xFFu) : (unsigned char)0;
         }
     }
-    finish_head_sum(s0 + s1, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
+    finish_head_sum(((dacc[0] + dacc[1]) + (dacc[2] + dacc[3])) * 0.125f, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
 }
 
 // Generic path: any d, any alignment; one thread per (row, u64 word), scalar loads.
