@@ -665,12 +665,12 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             mbar_init(&sm->kfree[s], 1);     // tcgen05.commit after the S MMA that read the stage
             mbar_init(&sm->vfull[s], 1);     // expect_tx arrive + TMA bytes
             mbar_init(&sm->vfree[s], 1);     // tcgen05.commit after the P.V MMA that read the stage
-            mbar_init(&sm->bfull[s], BIAS == 3 ? 2 : 1);  // expect_tx arrive + TMA bytes, or one arrival per expander warp (window)
+            mbar_init(&sm->bfull[s], BIAS == 3 ? 64 : 1);  // expect_tx arrive + TMA bytes, or one arrival per expander thread (window)
             mbar_init(&sm->bfree[s], 4);     // one elected arrival per softmax warp (bias stage read out)
         }
         mbar_init(&sm->ofree, 4);            // one elected arrival per softmax warp (O read out by the epilogue)
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm->ffull[s], 1);     // the first expander warp (it owns keys 0..7 past the last full tile)
+            mbar_init(&sm->ffull[s], kFoldMax);  // one arrival per writing lane of the first expander warp (keys 0..7 past the last full tile)
             mbar_init(&sm->ffree[s], 4);     // one elected arrival per softmax warp
         }
         fence_barrier_init();
@@ -848,8 +848,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
                             const uint32_t hi = 2 * w + 1 < KPAD / 32 ? wf[(2 * w + 1) % (KPAD / 32)] : 0u;
                             sm->kbits[fr.stage][t][w] = ((uint64_t)hi << 32) | lo;
                         }
+                        mbar_arrive(&sm->ffull[fr.stage]);  // each writer releases its own words (keeps racecheck's model simple)
                     }
-                    warp_arrive(&sm->ffull[fr.stage], lane);
                     fr.next(2);
                     if (un < prm.units) load_words<KPAD>(wf, a.k_words + ((int64_t)hn * N + T * BN + t) * w64, w64, t < prm.fold);
                 }
@@ -885,7 +885,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
 #pragma unroll
                     for (int q = 0; q < PER; ++q)
                         if (t + 64 * q < kRelWin) win[t + 64 * q] = wv[q];
-                    warp_arrive(&sm->bfull[wr.stage], lane);
+                    mbar_arrive(&sm->bfull[wr.stage]);  // every writer releases its own entries
                     wr.next(prm.bst);
                 }
                 mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
