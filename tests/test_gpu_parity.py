@@ -493,3 +493,62 @@ def test_tensor_core_logits_bit_exact(ba, port, n, d):
         ba.lib.ba_debug_tcgen05_logits(None, -1)
     want = port.binary_gemm(port.pack_signs(heads[1][0]), port.pack_signs(heads[1][1]), d)
     assert np.array_equal(S.cpu().numpy(), want)
+
+
+def test_full_size_c4_properties(ba, port):
+    """BASELINE.json configs[3] (DiT-XL/2 at 512 px: B=32 H=16 N=1024 d=72, dense per-head bias) at full size: sampled
+    heads against the oracle, rows of P sum to one, linearity in V."""
+    import torch
+    B, H, n, d = 32, 16, 1024, 72
+    g = torch.Generator(device="cuda").manual_seed(4)
+    Q, K, V = (torch.randn(B, H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    bias = (0.5 * torch.randn(H, n, n, device="cuda", generator=g)).to(torch.bfloat16)
+    O = ba.forward(Q, K, V, bias)
+    assert torch.isfinite(O).all()
+    for (b, h) in [(0, 0), (13, 7), (31, 15)]:
+        f = lambda t: t[b, h].float().cpu().numpy().astype(np.float64)
+        y = port.binary_attention_fused(f(Q), f(K), f(V), bias=bias[h].float().cpu().numpy().astype(np.float64))[0]
+        assert np.abs(O[b, h].cpu().numpy() - y).max() <= TOL_O
+    ones = ba.forward(Q[:4], K[:4], torch.ones_like(V[:4]), bias)
+    assert (ones - 1.0).abs().max().item() <= 1e-3
+    V2 = torch.randn(4, H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    Vs = (V[:4].float() + V2.float()).to(torch.bfloat16)   # rounded sum: compare against the same rounded operand
+    lin = ba.forward(Q[:4], K[:4], Vs, bias) - (O[:4] + ba.forward(Q[:4], K[:4], V2, bias))
+    dv = (Vs.float() - V[:4].float() - V2.float()).abs().max().item()
+    assert lin.abs().max().item() <= dv + 2 * 1e-3         # O is linear in V up to V's own rounding and the bf16 weights
+
+
+@pytest.mark.parametrize("with_rel1d", [False, True])
+def test_full_size_c5_properties(ba, port, with_rel1d):
+    """BASELINE.json configs[4] at its largest point (B=1 H=16 N=16384 d=128): a whole-head oracle run would take minutes,
+    so sampled ROWS are checked against a row-wise numpy restatement of attention.cpp:289-364 fed the oracle's own sign
+    planes and scales (quantize.cpp:16-23), next to the size-independent properties."""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    B, H, n, d = 1, 16, 16384, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Q, K, V = (torch.randn(B, H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    offs = (0.5 * torch.randn(H, 2 * n - 1, device="cuda", generator=g)).to(torch.bfloat16).float() if with_rel1d else None
+    bias = pkg.Relative1dBias(offs) if with_rel1d else None
+    O = ba.forward(Q, K, V, bias)
+    assert torch.isfinite(O).all()
+    rng = np.random.default_rng(9)
+    for h in (0, 9, 15):
+        q, k, v = (t[0, h].float().cpu().numpy().astype(np.float64) for t in (Q, K, V))
+        (_, mu_q), (_, mu_k) = port.binary_quantize(q), port.binary_quantize(k)
+        sk = np.where(k >= 0.0, 1.0, -1.0)
+        for r in [0, n - 1] + [int(x) for x in rng.integers(0, n, size=3)]:
+            dot = sk @ np.where(q[r] >= 0.0, 1.0, -1.0)                       # integer-valued, exact in fp64
+            s = mu_q * mu_k * dot / np.sqrt(d)                                # attention.cpp:34-36
+            if with_rel1d:
+                s = s + offs[h].cpu().numpy().astype(np.float64)[r - np.arange(n) + n - 1]   # attention.cpp:65-76
+            p = np.exp(s - s.max())
+            y = (p / p.sum()) @ v
+            assert np.abs(O[0, h, r].cpu().numpy() - y).max() <= TOL_O
+    ones = ba.forward(Q[:, :2], K[:, :2], torch.ones_like(V[:, :2]),
+                      pkg.Relative1dBias(offs[:2]) if with_rel1d else None)
+    assert (ones - 1.0).abs().max().item() <= 1e-3
+    if not with_rel1d:
+        perm = torch.randperm(n, device="cuda", generator=g)
+        Op = ba.forward(Q[:, :2], K[:, :2][:, :, perm], V[:, :2][:, :, perm])
+        assert (Op - O[:, :2]).abs().max().item() <= TOL_O
