@@ -1175,7 +1175,12 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap this kernel's prologue with K1's tail
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
+    // Only for many-wave launches.  With few units per CTA the static unit assignment makes the runtime depend on WHICH two
+    // CTAs share an SM: a normal launch places CTA b and b + #SMs together, which pairs a CTA that has one unit more with one
+    // that has one less (the survivor then finishes alone, up to 1.8x faster); a programmatic launch fills SMs as K1's CTAs
+    // retire and pairs neighbours instead -- measured 7-12% slower at 1024 units (3.46 per CTA), 1-2.6% faster at >= 6.9.
+    const long pdl_default = prm.units >= 6L * grid ? 1 : 0;
+    cfg.numAttrs = env_long("BA_PDL", pdl_default) ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL>, prm, m.v, m.b, m.o, m.v16);
     return e == cudaSuccess ? 1 : -(int)e;
 }
