@@ -1,3 +1,5 @@
+"""Dev tool: forward() per call with an L2 flush between calls (median/min) and back to back, for a few long shapes
+(used to find the programmatic-launch regression at 3.46 units per CTA; BA_PDL=0/1 overrides the policy)."""
 import sys, torch
 sys.path.insert(0, ".")
 import paper_2603_09582_b200 as pkg
