@@ -59,7 +59,6 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
     prm.o_vec8 = reinterpret_cast<uintptr_t>(a.O) % 32 == 0 ? 1 : 0;  // d % 8 == 0 keeps every row 32-byte aligned
-    if (env_long("BA_EXP_NOSTORE", 0)) prm.o_vec8 = 2;  // dev experiment: skip the O stores
     prm.dbg_S = g_dbg_S;
     prm.dbg_head = g_dbg_head;
     prm.dbg_T = g_dbg_T;
