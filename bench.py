@@ -370,7 +370,10 @@ def main():
                  "path": {"algorithmic_bytes": path_bytes, "ms": k1_ms + k2_ms,
                           "achieved_gbs": path_bytes / ((k1_ms + k2_ms) / 1e3) / 1e9 if k1_ms + k2_ms > 0 else None,
                           "frac_hbm": path_bytes / ((k1_ms + k2_ms) / 1e3) / 1e9 / pk["hbm_gbs"] if k1_ms + k2_ms > 0 else None},
-                 "mufu_exp_floor_ms": BH * N * N / 4.65e12 * 1e3})
+                 "mufu_exp_floor_ms": BH * N * N / 4.65e12 * 1e3,
+                 "events": "CUDA events recorded by the C ABI on the launching stream around K1 and K2 in a second pass of "
+                           "the same K steps right after the timed region (an event between the two kernels would defeat "
+                           "their programmatic overlap inside the timed steps); averaged over the K launches"})
 
     dense = None if args.no_dense else time_dense_bf16(Q, K, V, bias, min(args.steps, 20))
     cpu = None
