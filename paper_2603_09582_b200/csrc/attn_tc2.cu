@@ -1,0 +1,81 @@
+// attn_tc2.cu -- host side of the second-generation K2 (attn_tc2.cuh): shape gate, ring depths, tensor maps, dispatch.
+#include "attn_tc2.cuh"
+
+namespace ba {
+
+namespace tc {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_fn();  // attn_tcgen05.cu
+}  // namespace tc
+
+// Returns the number of kernels launched (> 0), a negative cudaError_t, or 0 when this kernel does not take the shape
+// (the caller then runs the first-generation kernel).
+int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, cudaStream_t stream) {
+    using namespace tc2;
+    if (env_long("BA_TC2", 1) == 0) return 0;
+    if (a.N % TN != 0 || a.N < 2 * TN) return 0;
+    if (a.d % 8 != 0 || a.d > 128) return 0;
+    if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 32 != 0) return 0;
+    int bias_mode = 0;
+    if (a.bias) {
+        if (a.bias_kind != BA_BIAS_DENSE) return 0;
+        const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 && reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
+        if (!tma_ok) return 0;
+        bias_mode = 1;
+    }
+    tc::EncodeTiledFn enc = tc::get_encode_fn();
+    if (!enc) return 0;
+    Params2 prm{};
+    prm.a = a;
+    prm.tiles = a.N / TN;
+    prm.ublocks = (a.N + 2 * TM - 1) / (2 * TM);
+    prm.units = a.BH * prm.ublocks;
+    prm.dvp = (a.d + 15) / 16 * 16;
+    prm.nbox = (a.d + 63) / 64;
+    prm.dbg_S = dbg_S;
+    prm.dbg_head = dbg_head;
+    const int kpad = (a.d + 31) / 32 * 32;
+    // ring depths: as deep as 227 KB allow; the bias ring must cover the HBM latency of the N x N stream
+    prm.kst = 2;
+    prm.vst = 3;
+    prm.qst = 2;
+    prm.bst = bias_mode ? 6 : 0;
+    if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 5) prm.bst = 5;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.vst = 2;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.qst = 1;
+    if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 4) prm.bst = 4;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) return 0;
+
+    CUtensorMap vmap, bmap;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    {
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 2, (cuuint64_t)a.N * a.d * 2};
+        const cuuint32_t box[3] = {64, (cuuint32_t)TN, 1};
+        if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    }
+    bmap = vmap;
+    if (bias_mode == 1) {
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.N, (cuuint64_t)a.N, (cuuint64_t)a.bias_heads};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.bias_ld * 2, (cuuint64_t)a.N * a.bias_ld * 2};
+        const cuuint32_t box[3] = {64, (cuuint32_t)TM, 1};
+        if (enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.bias), gdim, gstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    }
+    switch (kpad) {
+        case 32: return launch_kpad2<32>(prm, bias_mode, vmap, bmap, stream);
+        case 64: return launch_kpad2<64>(prm, bias_mode, vmap, bmap, stream);
+        case 96: return launch_kpad2<96>(prm, bias_mode, vmap, bmap, stream);
+        case 128: return launch_kpad2<128>(prm, bias_mode, vmap, bmap, stream);
+    }
+    return 0;
+}
+
+}  // namespace ba

@@ -94,6 +94,9 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
 }
 // Bounded wait: a protocol bug traps (clean launch failure) after 2^26 polls -- each poll sleeps in hardware up to
 // kSuspendHint ns or until the barrier moves, so that is seconds -- instead of hanging the GPU.
+#ifndef BA_WAIT_SPINS
+#define BA_WAIT_SPINS (1u << 26)  // dev builds lower this (BA_NVCC_FLAGS=-DBA_WAIT_SPINS=...) so a deadlock traps in seconds
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done = 0, spins = 0;
@@ -106,7 +109,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity), "r"(kSuspendHint)
             : "memory");
         if (done) break;
-        if (++spins == (1u << 26)) __trap();
+        if (++spins == BA_WAIT_SPINS) __trap();
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
