@@ -12,7 +12,7 @@ EncodeTiledFn get_encode_fn();  // attn_tcgen05.cu
 
 // Returns the number of kernels launched (> 0), a negative cudaError_t, or 0 when this kernel does not take the shape
 // (the caller then runs the first-generation kernel).
-int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, cudaStream_t stream) {
+int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* dbg_T, cudaStream_t stream) {
     using namespace tc2;
     if (env_long("BA_TC2", 1) == 0) return 0;
     if (a.N % TN != 0 || a.N < 2 * TN) return 0;
@@ -36,15 +36,17 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, cudaStream_t
     prm.nbox = (a.d + 63) / 64;
     prm.dbg_S = dbg_S;
     prm.dbg_head = dbg_head;
+    prm.dbg_T = dbg_T;
     const int kpad = (a.d + 31) / 32 * 32;
     // ring depths: as deep as 227 KB allow; the bias ring must cover the HBM latency of the N x N stream
-    prm.kst = 2;
-    prm.vst = 3;
+    prm.kst = 4;
+    prm.vst = 4;
     prm.qst = 2;
     prm.bst = bias_mode ? 6 : 0;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.kst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 5) prm.bst = 5;
-    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.vst = 2;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.qst = 1;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.vst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 4) prm.bst = 4;
     if (smem_bytes2(prm, kpad) > kSmemMax2) return 0;
 

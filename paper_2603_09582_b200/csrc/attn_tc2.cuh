@@ -1,5 +1,5 @@
 // attn_tc2.cuh -- K2, second generation: fused BinaryAttention forward for sm_100a with ONE CTA per SM that keeps two
-// 128-row query tiles in flight against 128-key tiles.
+// 128-row query tiles in flight and FOUR softmax warps on every scheduler.
 //
 // Same arithmetic as attn_tcgen05.cuh (binattn::binary_attention_fused, quantize_pv = false, proj/src/attention.cpp:250-382):
 //   S = Q^ K^T   exact +-1 contraction on tcgen05.mma.kind::f8f6f4 (== d - 2 popc(q xor k), bitops.cpp:59-67)
@@ -10,15 +10,18 @@
 // timeline shows a 64-key tile costing ~2000 clk per warp, half of it outside the exponentials (barrier round trips,
 // TMEM load/store waits, instruction fetch), so the MUFU pipe -- the floor of this kernel -- is ~50% busy.  A register
 // loop of the same instructions reaches 15.9 of 16 ex2/clk/SM with two warps per scheduler (scripts/micro/pipe_bench.cu).
-// This kernel therefore puts FOUR softmax warps on every scheduler:
 //   unit        = (head, 256 query rows) = query tiles A and B; both use the same expanded K tile and the same V tile
-//   softmax     = 16 warps: (tile A | B) x (key columns 0-63 | 64-127) x 4 lane quadrants; thread = one row x 64 keys
-//   per tile    = one S wait, one P hand-over and one P.V commit per 128 keys (half the fixed cost of 64-key tiles)
-//   MMA order   = PV_A(j-1), S_A(j), PV_B(j-1), S_B(j): tile A computes its softmax while the tensor core works for
-//                 tile B and vice versa, so the MUFU pipe always sees two warps per scheduler in their exp phase
-// 640 threads: warps 0-15 softmax (104 registers), 16 MMA issue + TMEM allocation, 17 TMA producer, 18-19 Q/K expanders.
-// TMEM (512 columns): S_A [0,128) | S_B [128,256) | O_A [256,256+dvp) | O_B [384,384+dvp); the bf16 weights overwrite the
-// S columns their thread has just read: keys 0-63 -> columns [0,32), keys 64-127 -> columns [64,96) of the tile's S block.
+//   key tiles   = 64 keys; every query tile has TWO S stages in tensor memory, and the S MMA of tile j+1 is issued before
+//                 the P.V MMA of tile j, so a softmax warp never waits for the tensor core
+//   softmax     = 16 warps: (tile A | B) x (key columns 0-31 | 32-63) x 4 lane quadrants; thread = one row x 32 keys;
+//                 the fixed per-tile cost of one warp (barrier, TMEM load / store round trips) hides behind the
+//                 exponentials of the three other warps of its scheduler
+//   (a first version used 128-key tiles with one S stage per query tile and 64 keys per thread; the two query tiles then
+//    ran in phase -- both waiting for the tensor core at the same time -- and the MUFU pipe stayed at 64%)
+// 640 threads: warps 0-15 softmax (104 registers), 16 / 17 MMA issue for tile A / B (16 also allocates TMEM), 18 TMA producer,
+// 19 Q/K expander.
+// TMEM (512 columns): tile X owns S stages [128 X + 64 s, +64) and O [256 + 128 X, +dvp); the bf16 weights overwrite the
+// S columns their thread has just read: keys 0-31 -> columns [0,16), keys 32-63 -> columns [32,48) of the stage.
 //
 // Reference max.  The running max follows the lazy rule of the first kernel (O and l are rescaled only when a row max
 // grows by more than 2^kThr2 over the reference used so far; O / l is unaffected).  The two threads of a row exchange a
@@ -35,11 +38,11 @@ namespace tc2 {
 using namespace ba::tc;  // PTX wrappers, descriptors, Ring, expand_store, rescale_o
 
 constexpr int TM = 128;            // rows of one query tile (UMMA M)
-constexpr int TN = 128;            // keys per tile (UMMA N of the S MMA)
+constexpr int TN = 64;             // keys per tile (UMMA N of the S MMA)
 constexpr int kThreads2 = 640;
 constexpr int kColO2 = 256;        // first O column; tile X owns [256 + 128 X, +dvp)
-constexpr int kVBox = 16384;       // one TMA box of V: 128 keys x 64 columns bf16, 128B swizzle
-constexpr int kBSub = 16384;       // one bias sub-tile: 128 rows x 64 columns bf16, 128B swizzle
+constexpr int kVBox = 8192;        // one TMA box of V: 64 keys x 64 columns bf16, 128B swizzle
+constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16, 128B swizzle
 constexpr float kThr2 = 16.0f;     // lazy-rescale threshold, log2 units
 constexpr float kFastBound = 32.0f;  // FAST path when d * mu_q mu_k / tau * log2(e) <= this (weights stay >= 2^-64)
 constexpr int kRegsSoftmax2 = 104, kRegsCtrl2 = 64;  // the pool is what the launch allocated: 640 x 96 = 512 x 104 + 128 x 64
@@ -48,12 +51,11 @@ struct Smem2 {
     uint64_t qfull[2], qfree[2];  // Q tiles of a unit expanded / every S MMA of the unit retired
     uint64_t kfull[4], kfree[4];  // K tile expanded / its S MMAs retired
     uint64_t vfull[4], vfree[4];  // V tile landed (TMA) / its P.V MMAs retired
-    uint64_t bfull[8], bfree[8];  // bias sub-tile landed (TMA) / read out by its four softmax warps
-    uint64_t sfull[2];            // S of query tile X ready in TMEM
-    uint64_t pfull[2];            // P of query tile X written by its eight softmax warps
-    uint64_t pvdone[2];           // P.V MMA of query tile X retired
+    uint64_t bfull[8], bfree[8];  // bias tile landed (TMA) / read out by the eight softmax warps of its query tile
+    uint64_t sfull[2][2];         // [query tile][stage] S ready in TMEM
+    uint64_t pfull[2][2];         // [query tile][stage] P written by the eight softmax warps of the query tile
+    uint64_t pvdone[2][2];        // [query tile][stage] P.V MMA retired
     uint64_t ofree[2];            // O of query tile X read out by the epilogue
-    uint64_t stag;                // tile A is half way through its first softmax tile: S_B(0) may be issued (phase stagger)
     uint2 lut[256];               // byte of sign bits -> 8 e4m3 +-1.0 bytes
     float xch[2][2][TM];          // (query tile, column half, row): half-row max / partial denominator for the other half
     uint32_t flag[2][2][4][2];    // (tile parity, query tile, lane quadrant, column half): "my warp needs a new reference max"
@@ -62,7 +64,7 @@ struct Smem2 {
 
 struct Params2 {
     FwdArgs a;
-    int tiles;     // N / 128 key tiles
+    int tiles;     // N / 64 key tiles
     int ublocks;   // ceil(N / 256) units per head
     int units;     // BH * ublocks
     int dvp;       // d rounded up to 16
@@ -70,6 +72,7 @@ struct Params2 {
     int qst, kst, vst, bst;
     int32_t* dbg_S;
     int dbg_head;
+    long long* dbg_T;
 };
 
 __device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1) {
@@ -80,42 +83,54 @@ __device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1) {
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-// BIAS: 0 = none, 1 = dense bf16 table staged by TMA.  N % 128 == 0.
-template <int KPAD, int BIAS, bool DBG>
+// BIAS: 0 = none, 1 = dense bf16 table staged by TMA.  N % 64 == 0.
+#define BA_STAMP2()                                                      \
+    do {                                                                 \
+        if (TL && tl_buf && tl_n < kTlStamps) tl_buf[tl_n++] = clock64(); \
+    } while (0)
+
+template <int KPAD, int BIAS, bool DBG, bool TL = false>
 __global__ void __launch_bounds__(kThreads2, 1)
 attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUtensorMap vmap,
                 const __grid_constant__ CUtensorMap bmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
-    unsigned char* sV = smem_raw;                               // vst x nbox x 16 KB
+    unsigned char* sV = smem_raw;                               // vst x nbox x 8 KB
     unsigned char* sB = sV + prm.vst * prm.nbox * kVBox;        // bst x 16 KB
     unsigned char* sQ = sB + prm.bst * kBSub;                   // qst x 256 x KPAD (tile A rows, then tile B rows)
-    unsigned char* sK = sQ + prm.qst * 2 * TM * KPAD;           // kst x 128 x KPAD
+    unsigned char* sK = sQ + prm.qst * 2 * TM * KPAD;           // kst x 64 x KPAD
     Smem2* sm = reinterpret_cast<Smem2*>(sK + prm.kst * TN * KPAD);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = a.N, d = a.d, w64 = a.W64, T = prm.tiles;
     const int G = gridDim.x;
+    // dev timeline (TL builds): [cta][role 0 = softmax warp 0 (tile A), 1 = MMA warp, 2 = TMA lane, 3 = expander][kTlStamps]
+    long long* tl_buf = nullptr;
+    int tl_n = 0;
+    (void)tl_n;
+    if (TL && prm.dbg_T && (tid == 0 || tid == 512 || tid == 544 || tid == 608))
+        tl_buf = prm.dbg_T + ((size_t)blockIdx.x * 4 + (tid == 0 ? 0 : tid == 512 ? 1 : tid == 544 ? 2 : 3)) * kTlStamps;
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm->qfull[s], 2);
-            mbar_init(&sm->qfree[s], 1);
-            mbar_init(&sm->sfull[s], 1);
-            mbar_init(&sm->pfull[s], 8);
-            mbar_init(&sm->pvdone[s], 1);
+            mbar_init(&sm->qfull[s], 1);
+            mbar_init(&sm->qfree[s], 2);
             mbar_init(&sm->ofree[s], 8);
+            for (int t = 0; t < 2; ++t) {
+                mbar_init(&sm->sfull[s][t], 1);
+                mbar_init(&sm->pfull[s][t], 8);
+                mbar_init(&sm->pvdone[s][t], 1);
+            }
         }
-        mbar_init(&sm->stag, 8);
         for (int s = 0; s < 4; ++s) {
-            mbar_init(&sm->kfull[s], 2);
-            mbar_init(&sm->kfree[s], 1);
+            mbar_init(&sm->kfull[s], 1);
+            mbar_init(&sm->kfree[s], 2);
             mbar_init(&sm->vfull[s], 1);
-            mbar_init(&sm->vfree[s], 1);
+            mbar_init(&sm->vfree[s], 2);
         }
         for (int s = 0; s < 8; ++s) {
             mbar_init(&sm->bfull[s], 1);
-            mbar_init(&sm->bfree[s], 4);
+            mbar_init(&sm->bfree[s], 8);
         }
         fence_barrier_init();
     }
@@ -124,7 +139,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (warp == 17 && lane == 0) {
+    if (warp == 18 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
         if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
     }
@@ -137,101 +152,117 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
 
     if (warp >= 16) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtrl2));
-        if (warp == 16) {
-            // ======================================================== MMA issuer (whole warp, one elected lane issues)
+        if (warp <= 17) {
+            // ======================================================== MMA issuers: warp 16 for query tile A, warp 17 for tile B
+            // (whole warp, one elected lane issues).  One warp issuing for both tiles was the bottleneck of the first build of
+            // this kernel: its serial chain of barrier polls (~250 clk each) and descriptor set-up took ~1900 clk per key tile
+            // against 1024 clk of exponentials.  Each warp polls all barriers of an iteration up front (the predicates land
+            // asynchronously) and only falls back to a blocking wait for the ones still open.
+            const int X = warp - 16;
             const uint32_t idesc_s = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
             const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(prm.dvp >> 3) << 17) |
                                       ((uint32_t)(TM >> 4) << 24);
-            const uint64_t q_desc = make_desc(smem_u32(sQ), TM * 16, 128, 0);
+            const uint64_t q_desc = make_desc(smem_u32(sQ) + X * TM * KPAD, TM * 16, 128, 0);
             const uint64_t k_desc = make_desc(smem_u32(sK), TN * 16, 128, 0);
             const uint64_t v_desc = make_desc(smem_u32(sV), kVBox, 1024, 2);
+            const uint32_t s_tmem = tmem + X * 128, o_tmem = tmem + kColO2 + X * 128;
             Ring qr, kr, vr;
-            uint32_t gp[2] = {0, 0};  // P tiles consumed per query tile
-            uint32_t up[2] = {0, 0};  // units finished per query tile
-            int pend = 0, pj = 0, pnact = 0, pvs = 0;
-            bool staggered = false;
+            uint32_t g = 0;   // key tiles of my query tile issued so far (S stage = g & 1); P.V runs one tile behind
+            uint32_t up = 0;  // units of my query tile whose last P.V has been issued
+            int pend = 0, pj = 0, pact = 0, pvs = 0;
             uint32_t pvph = 0;
-            // P.V of the pending key tile for query tile X (issued one S MMA late, see the header)
-            auto issue_pv = [&](int X, bool last_of_tile) {
-                mbar_wait(&sm->pfull[X], gp[X] & 1u);
-                if (pj == 0 && up[X] > 0) mbar_wait(&sm->ofree[X], (up[X] - 1) & 1u);  // the epilogue has read the old O
-                tc_fence_after();
-                const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * kVBox) >> 4);
-                const uint32_t p_tmem = tmem + X * TN;
-                if (elect_one()) {
-#pragma unroll
-                    for (int ks = 0; ks < TN / 16; ++ks)
-                        mma_bf16_ts(tmem + kColO2 + X * 128, p_tmem + (ks >> 2) * 64 + (ks & 3) * 8, vd + (uint64_t)(ks * (2048 >> 4)),
-                                    idesc_pv, (pj > 0 || ks > 0) ? 1u : 0u);
-                    tc_commit(&sm->pvdone[X]);
-                    if (last_of_tile) tc_commit(&sm->vfree[pvs]);
-                }
-                __syncwarp();
-                ++gp[X];
-                if (pj == T - 1) ++up[X];
-            };
             for (int u = blockIdx.x; u < prm.units; u += G) {
                 const int ub = u % prm.ublocks;
-                const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
+                const int act = (X == 0 || ub * 2 * TM + TM < N) ? 1 : 0;  // tile B of a head's last unit may be empty: keep the rings moving
                 mbar_wait(&sm->qfull[qr.stage], qr.phase);
                 const uint64_t qd = q_desc + (uint64_t)((qr.stage * 2 * TM * KPAD) >> 4);
                 for (int j = 0; j < T; ++j) {
+                    const uint32_t pst = (g - 1) & 1u;  // stage of the pending tile (when there is one)
+                    const uint32_t k_ok = mbar_test(&sm->kfull[kr.stage], kr.phase);  // (test_wait: try_wait may sleep on an open phase)
+                    uint32_t v_ok = 1, p_ok = 1;
                     if (pend) {
-                        mbar_wait(&sm->vfull[pvs], pvph);
-                        issue_pv(0, pnact == 1);
+                        v_ok = mbar_test(&sm->vfull[pvs], pvph);
+                        if (pact) p_ok = mbar_test(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
                     }
-                    mbar_wait(&sm->kfull[kr.stage], kr.phase);
-                    tc_fence_after();
-                    const uint64_t kd = k_desc + (uint64_t)((kr.stage * TN * KPAD) >> 4);
-                    if (elect_one()) {
-#pragma unroll
-                        for (int ks = 0; ks < KPAD / 32; ++ks)
-                            mma_f8(tmem, qd + (uint64_t)(ks * ((2 * TM * 16) >> 4)), kd + (uint64_t)(ks * ((2 * TN * 16) >> 4)), idesc_s,
-                                   ks > 0 ? 1u : 0u);
-                        tc_commit(&sm->sfull[0]);
-                        if (nact == 1) {
-                            tc_commit(&sm->kfree[kr.stage]);
-                            if (j == T - 1) tc_commit(&sm->qfree[qr.stage]);
-                        }
-                    }
-                    __syncwarp();
-                    if (pend && pnact == 2) issue_pv(1, true);
-                    if (nact == 2) {
-                        // The two query tiles must run in ANTI-phase (A in its exponentials while the tensor core works for
-                        // B): the offset between them is neutrally stable, so it is set once, here, by holding B's first S
-                        // back until A is half way through its first tile.
-                        if (!staggered) {
-                            mbar_wait(&sm->stag, 0);
-                            staggered = true;
-                        }
+                    if (!k_ok) mbar_wait(&sm->kfull[kr.stage], kr.phase);
+                    BA_STAMP2();
+                    if (act) {
+                        tc_fence_after();
+                        const uint64_t kd = k_desc + (uint64_t)((kr.stage * TN * KPAD) >> 4);
                         if (elect_one()) {
 #pragma unroll
                             for (int ks = 0; ks < KPAD / 32; ++ks)
-                                mma_f8(tmem + TN, qd + (uint64_t)((TM * KPAD) >> 4) + (uint64_t)(ks * ((2 * TM * 16) >> 4)),
+                                mma_f8(s_tmem + (g & 1u) * TN, qd + (uint64_t)(ks * ((2 * TM * 16) >> 4)),
                                        kd + (uint64_t)(ks * ((2 * TN * 16) >> 4)), idesc_s, ks > 0 ? 1u : 0u);
-                            tc_commit(&sm->sfull[1]);
+                            tc_commit(&sm->sfull[X][g & 1u]);
                             tc_commit(&sm->kfree[kr.stage]);
                             if (j == T - 1) tc_commit(&sm->qfree[qr.stage]);
                         }
                         __syncwarp();
+                    } else if (lane == 0) {
+                        mbar_arrive(&sm->kfree[kr.stage]);
+                        if (j == T - 1) mbar_arrive(&sm->qfree[qr.stage]);
+                    }
+                    BA_STAMP2();
+                    if (pend) {
+                        if (!v_ok) mbar_wait(&sm->vfull[pvs], pvph);
+                        if (pact) {
+                            if (!p_ok) mbar_wait(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
+                            if (pj == 0 && up > 0) mbar_wait(&sm->ofree[X], (up - 1) & 1u);  // the epilogue has read the old O
+                            BA_STAMP2();
+                            tc_fence_after();
+                            const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * kVBox) >> 4);
+                            const uint32_t p_tmem = s_tmem + pst * TN;
+                            if (elect_one()) {
+#pragma unroll
+                                for (int ks = 0; ks < TN / 16; ++ks)
+                                    mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
+                                                (pj > 0 || ks > 0) ? 1u : 0u);
+                                tc_commit(&sm->pvdone[X][pst]);
+                                tc_commit(&sm->vfree[pvs]);
+                            }
+                            __syncwarp();
+                            BA_STAMP2();
+                            if (pj == T - 1) ++up;
+                        } else if (lane == 0) {
+                            mbar_arrive(&sm->vfree[pvs]);
+                        }
                     }
                     pend = 1;
                     pj = j;
-                    pnact = nact;
+                    pact = act;
                     pvs = vr.stage;
                     pvph = vr.phase;
                     vr.next(prm.vst);
                     kr.next(prm.kst);
+                    if (act) ++g;
                 }
                 qr.next(prm.qst);
             }
-            if (pend) {
+            if (pend) {  // the last tile's P.V
                 mbar_wait(&sm->vfull[pvs], pvph);
-                issue_pv(0, pnact == 1);
-                if (pnact == 2) issue_pv(1, true);
+                if (pact) {
+                    const uint32_t pst = (g - 1) & 1u;
+                    mbar_wait(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
+                    if (pj == 0 && up > 0) mbar_wait(&sm->ofree[X], (up - 1) & 1u);
+                    tc_fence_after();
+                    const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * kVBox) >> 4);
+                    const uint32_t p_tmem = s_tmem + pst * TN;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int ks = 0; ks < TN / 16; ++ks)
+                            mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
+                                        (pj > 0 || ks > 0) ? 1u : 0u);
+                        tc_commit(&sm->pvdone[X][pst]);
+                        tc_commit(&sm->vfree[pvs]);
+                    }
+                    __syncwarp();
+                } else if (lane == 0) {
+                    mbar_arrive(&sm->vfree[pvs]);
+                }
             }
-        } else if (warp == 17) {
-            // ======================================================== TMA producer: bias sub-tiles, V tiles
+        } else if (warp == 18) {
+            // ======================================================== TMA producer: bias tiles, V tiles
             if (lane == 0) {
                 Ring vr, br;
                 for (int u = blockIdx.x; u < prm.units; u += G) {
@@ -241,11 +272,10 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     const int bh = (a.head0 + head) % a.H % a.bias_heads;
                     for (int j = 0; j < T; ++j) {
                         if (BIAS == 1) {
-                            for (int s = 0; s < 2 * nact; ++s) {  // (tile A | B) x (columns 0-63 | 64-127), in consumption order
+                            for (int X = 0; X < nact; ++X) {
                                 mbar_wait(&sm->bfree[br.stage], br.phase ^ 1u);
                                 mbar_expect_tx(&sm->bfull[br.stage], kBSub);
-                                tma_load_3d(&bmap, &sm->bfull[br.stage], sB + br.stage * kBSub, j * TN + (s & 1) * 64,
-                                            ub * 2 * TM + (s >> 1) * TM, bh);
+                                tma_load_3d(&bmap, &sm->bfull[br.stage], sB + br.stage * kBSub, j * TN, ub * 2 * TM + X * TM, bh);
                                 br.next(prm.bst);
                             }
                         }
@@ -258,72 +288,83 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 }
             }
         } else {
-            // ======================================================== Q / K expanders (64 threads)
-            const int t = tid - 18 * 32;
+            // ======================================================== Q / K expander (one warp: two keys per lane and tile)
             Ring qr, kr;
             uint32_t wk0[KPAD / 32], wk1[KPAD / 32];
             if ((int)blockIdx.x < prm.units) {
                 const int head = blockIdx.x / prm.ublocks;
-                load_words<KPAD>(wk0, a.k_words + ((int64_t)head * N + t) * w64, w64, true);
-                load_words<KPAD>(wk1, a.k_words + ((int64_t)head * N + t + 64) * w64, w64, true);
+                load_words<KPAD>(wk0, a.k_words + ((int64_t)head * N + lane) * w64, w64, true);
+                load_words<KPAD>(wk1, a.k_words + ((int64_t)head * N + lane + 32) * w64, w64, true);
             }
             for (int u = blockIdx.x; u < prm.units; u += G) {
                 const int head = u / prm.ublocks;
                 const int row0 = (u - head * prm.ublocks) * 2 * TM;
-                {   // the unit's 256 query rows (rows past N expand to zeros)
-                    uint32_t wq[4][KPAD / 32];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        load_words<KPAD>(wq[i], a.q_words + ((int64_t)head * N + row0 + t + 64 * i) * w64, w64, row0 + t + 64 * i < N);
-                    mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
-                    unsigned char* qt = sQ + qr.stage * 2 * TM * KPAD;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        expand_store<KPAD>(qt + (i >> 1) * TM * KPAD, TM, t + 64 * (i & 1), wq[i], d, row0 + t + 64 * i < N, sm->lut);
-                    fence_proxy_async();
-                    warp_arrive(&sm->qfull[qr.stage], lane);
-                    qr.next(prm.qst);
+                mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
+                unsigned char* qt = sQ + qr.stage * 2 * TM * KPAD;
+#pragma unroll 1
+                for (int i = 0; i < 8; i += 2) {  // the unit's 256 query rows, two per lane and pass (rows past N expand to zeros)
+                    uint32_t wq0[KPAD / 32], wq1[KPAD / 32];
+                    const int r0 = lane + 32 * i, r1 = r0 + 32;
+                    load_words<KPAD>(wq0, a.q_words + ((int64_t)head * N + row0 + r0) * w64, w64, row0 + r0 < N);
+                    load_words<KPAD>(wq1, a.q_words + ((int64_t)head * N + row0 + r1) * w64, w64, row0 + r1 < N);
+                    expand_store<KPAD>(qt + (r0 >> 7) * TM * KPAD, TM, r0 & 127, wq0, d, row0 + r0 < N, sm->lut);
+                    expand_store<KPAD>(qt + (r1 >> 7) * TM * KPAD, TM, r1 & 127, wq1, d, row0 + r1 < N, sm->lut);
                 }
+                fence_proxy_async();
+                warp_arrive(&sm->qfull[qr.stage], lane);
+                qr.next(prm.qst);
                 const int un = u + G;
                 const int hn = un / prm.ublocks;
                 for (int j = 0; j < T; ++j) {
+                    // the next tile's words are requested BEFORE this tile is expanded (the next unit's first tile after the
+                    // last one): their L2 / HBM latency hides behind the expansion and the wait for a free stage
+                    uint32_t nk0[KPAD / 32], nk1[KPAD / 32];
+                    if (j + 1 < T) {
+                        load_words<KPAD>(nk0, a.k_words + ((int64_t)head * N + (j + 1) * TN + lane) * w64, w64, true);
+                        load_words<KPAD>(nk1, a.k_words + ((int64_t)head * N + (j + 1) * TN + lane + 32) * w64, w64, true);
+                    } else {
+                        load_words<KPAD>(nk0, a.k_words + ((int64_t)hn * N + lane) * w64, w64, un < prm.units);
+                        load_words<KPAD>(nk1, a.k_words + ((int64_t)hn * N + lane + 32) * w64, w64, un < prm.units);
+                    }
                     mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
+                    BA_STAMP2();
                     unsigned char* kt = sK + kr.stage * TN * KPAD;
-                    expand_store<KPAD>(kt, TN, t, wk0, d, true, sm->lut);
-                    expand_store<KPAD>(kt, TN, t + 64, wk1, d, true, sm->lut);
+                    expand_store<KPAD>(kt, TN, lane, wk0, d, true, sm->lut);
+                    expand_store<KPAD>(kt, TN, lane + 32, wk1, d, true, sm->lut);
                     fence_proxy_async();
                     warp_arrive(&sm->kfull[kr.stage], lane);
+                    BA_STAMP2();
                     kr.next(prm.kst);
-                    if (j + 1 < T) {
-                        load_words<KPAD>(wk0, a.k_words + ((int64_t)head * N + (j + 1) * TN + t) * w64, w64, true);
-                        load_words<KPAD>(wk1, a.k_words + ((int64_t)head * N + (j + 1) * TN + t + 64) * w64, w64, true);
-                    } else if (un < prm.units) {
-                        load_words<KPAD>(wk0, a.k_words + ((int64_t)hn * N + t) * w64, w64, true);
-                        load_words<KPAD>(wk1, a.k_words + ((int64_t)hn * N + t + 64) * w64, w64, true);
+#pragma unroll
+                    for (int i = 0; i < KPAD / 32; ++i) {
+                        wk0[i] = nk0[i];
+                        wk1[i] = nk1[i];
                     }
                 }
             }
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax2));
-        // ============================================================ softmax + epilogue: thread = (query row, 64 keys)
+        // ============================================================ softmax + epilogue: thread = (query row, 32 keys)
         const int X = warp >> 3, half = (warp >> 2) & 1, quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-        const uint32_t s_addr = lane_base + X * TN + half * 64;  // my 64 S columns; P goes over the first 32 of them
+        const uint32_t s_base = lane_base + X * 128 + half * 32;  // + 64 * stage: my 32 S columns; P goes over the first 16
         const uint32_t o_addr = lane_base + kColO2 + X * 128;
         const int pair_id = 1 + X * 4 + quad;
         const int h16 = ((prm.dvp >> 1) + 15) & ~15;             // O columns [0,h16) belong to half 0, [h16,dvp) to half 1
         const int oc0 = half ? h16 : 0, oc1 = half ? prm.dvp : h16;
         const bool stats = a.row_max != nullptr || a.row_sum != nullptr;
-        uint32_t gx = 0;      // key tiles this query tile has been through (parity of sfull / pfull / pvdone)
-        uint32_t bcount = 0;  // bias sub-tiles the producer has issued before the current unit
+        uint32_t gx = 0;  // key tiles this query tile has been through (stage = gx & 1, parity = (gx >> 1) & 1)
+        Ring br;          // position of my query tile's next bias tile in the producer's ring
+        if (BIAS == 1 && X == 1) br.next(prm.bst);
         for (int u = blockIdx.x; u < prm.units; u += G) {
             const int head = u / prm.ublocks;
             const int ub = u - head * prm.ublocks;
             const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
             if (X >= nact) {  // tile B of the last unit of a head with an odd number of 128-row blocks: nothing to do
-                bcount += (uint32_t)(T * 2 * nact);
+                if (BIAS == 1)
+                    for (int j = 0; j < T; ++j) br.next(prm.bst);
                 continue;
             }
             const int row = ub * 2 * TM + X * TM + r;
@@ -333,44 +374,46 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             float m_ref = fast ? sc * kLog2e * (float)d : -INFINITY, m_true = -INFINITY;
             float l0 = 0.f, l1 = 0.f;
             const bool dump = DBG && prm.dbg_S && head == prm.dbg_head;
+            float x[32];
+            bool have = false;  // x already holds (or is being loaded with) the scores of the tile about to be processed
             for (int j = 0; j < T; ++j, ++gx) {
-                float x[64];
-                uint32_t bstage = 0;
-                mbar_wait(&sm->sfull[X], gx & 1u);
-                tc_fence_after();
-                BA_TMEM_LD16(s_addr + 0, x, 0);
-                BA_TMEM_LD16(s_addr + 16, x, 16);
-                BA_TMEM_LD16(s_addr + 32, x, 32);
-                BA_TMEM_LD16(s_addr + 48, x, 48);
-                if (BIAS == 1) {
-                    const uint32_t bi = bcount + (uint32_t)(j * 2 * nact + X * 2 + half);
-                    const uint32_t lap = bi / (uint32_t)prm.bst;
-                    bstage = bi - lap * (uint32_t)prm.bst;
-                    mbar_wait(&sm->bfull[bstage], lap & 1u);
+                const uint32_t st = gx & 1u, par = (gx >> 1) & 1u;
+                const uint32_t s_addr = s_base + st * TN;
+                BA_STAMP2();
+                if (!have) {
+                    mbar_wait(&sm->sfull[X][st], par);
+                    tc_fence_after();
+                    BA_TMEM_LD16(s_addr + 0, x, 0);
+                    BA_TMEM_LD16(s_addr + 16, x, 16);
                 }
+                BA_STAMP2();
+                if (BIAS == 1) mbar_wait(&sm->bfull[br.stage], br.phase);
                 tc_wait_ld();
+                BA_STAMP2();
                 if (DBG && dump) {
-                    int32_t* drow = prm.dbg_S + (int64_t)row * N + j * TN + half * 64;
+                    int32_t* drow = prm.dbg_S + (int64_t)row * N + j * TN + half * 32;
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) drow[i] = (int)x[i];
+                    for (int i = 0; i < 32; ++i) drow[i] = (int)x[i];
                 }
                 if (BIAS == 1) {
-                    const unsigned char* brow = sB + bstage * kBSub + r * 128;  // row r of the 128 x 64 bf16 sub-tile
+                    const unsigned char* brow = sB + br.stage * kBSub + r * 128;  // row r of the 128 x 64 bf16 tile
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 b = *reinterpret_cast<const uint4*>(brow + ((c ^ (r & 7)) << 4));
+                    for (int c = 0; c < 4; ++c) {
+                        const uint4 b = *reinterpret_cast<const uint4*>(brow + (((half * 4 + c) ^ (r & 7)) << 4));
                         const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
                             fma2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], sc, sc,
                                  __uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xFFFF0000u));
                     }
-                    warp_arrive(&sm->bfree[bstage], lane);
+                    warp_arrive(&sm->bfree[br.stage], lane);
+                    br.next(prm.bst);  // tile A and tile B alternate in the ring when both are active
+                    if (nact == 2) br.next(prm.bst);
                 }
                 if (!fast) {
                     float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
 #pragma unroll
-                    for (int i = 4; i < 64; i += 4) {
+                    for (int i = 4; i < 32; i += 4) {
                         m0 = fmaxf(m0, x[i]);
                         m1 = fmaxf(m1, x[i + 1]);
                         m2 = fmaxf(m2, x[i + 2]);
@@ -389,37 +432,48 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         m_true = fmaxf(m_true, tm);
                         if (tm > m_ref + kThr2) {
                             const float alpha = ex2(m_ref - tm);  // first tile: 2^-inf = 0 on a still-unwritten O
-                            // S(j) is complete, so P.V(j-1) -- issued before it -- has retired: O is quiescent
-                            if (j > 0 && oc1 > oc0) rescale_o(o_addr + oc0, oc1 - oc0, alpha);
+                            if (j > 0 && oc1 > oc0) {
+                                // S(j) was issued BEFORE P.V(j-1): wait for that MMA before touching O.  Tile j-1 is this
+                                // barrier's previous use and tile j-3 (the one before) retired before S(j) did, so the
+                                // parity is unambiguous.
+                                mbar_wait(&sm->pvdone[X][st ^ 1u], ((gx - 1) >> 1) & 1u);
+                                rescale_o(o_addr + oc0, oc1 - oc0, alpha);
+                            }
                             l0 *= alpha;
                             l1 *= alpha;
                             m_ref = tm;
                         }
                     }
                 }
+                BA_STAMP2();
+                // ROLLING REFILL: if the next tile's S is already complete (the MMA warp runs a tile ahead), its scores are
+                // loaded into the registers of this tile's scores as soon as those have been through the exponent FMA, so the
+                // barrier and TMEM round trips of the next tile hide behind this tile's exponentials.
+                const bool nxt = j + 1 < T && mbar_test(&sm->sfull[X][st ^ 1u], ((gx + 1) >> 1) & 1u);
                 const float nm = -m_ref;
+                uint32_t pk[16];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int i = 32 * h + 2 * e;
-                        float a0, a1;
-                        fma2(a0, a1, x[i], x[i + 1], ea, ea, nm, nm);
-                        const float p0 = ex2(a0), p1 = ex2(a1);
-                        add2(l0, l1, p0, p1);
-                        pk[e] = pack_bf16(p0, p1);
+                for (int e = 0; e < 16; ++e) {
+                    float a0, a1;
+                    fma2(a0, a1, x[2 * e], x[2 * e + 1], ea, ea, nm, nm);
+                    const float p0 = ex2(a0), p1 = ex2(a1);
+                    add2(l0, l1, p0, p1);
+                    pk[e] = pack_bf16(p0, p1);
+                    if (e == 7 && nxt) {
+                        tc_fence_after();
+                        BA_TMEM_LD16(s_base + (st ^ 1u) * TN, x, 0);
                     }
-                    BA_TMEM_ST16U(s_addr + 16 * h, pk);
-                    if (h == 0 && X == 0 && gx == 0) warp_arrive(&sm->stag, lane);
+                    if (e == 15 && nxt) BA_TMEM_LD16(s_base + (st ^ 1u) * TN + 16, x, 16);
                 }
+                have = nxt;
+                BA_TMEM_ST16U(s_addr, pk);
+                BA_STAMP2();
                 tc_wait_st();
                 tc_fence_before();
-                warp_arrive(&sm->pfull[X], lane);
+                warp_arrive(&sm->pfull[X][st], lane);
             }
-            bcount += (uint32_t)(T * 2 * nact);
             // ---------------------------------------------------------------- epilogue: O / l for my half of the columns
-            mbar_wait(&sm->pvdone[X], (gx - 1) & 1u);
+            mbar_wait(&sm->pvdone[X][(gx - 1) & 1u], ((gx - 1) >> 1) & 1u);
             tc_fence_after();
             sm->xch[X][half][r] = l0 + l1;
             pair_sync(pair_id);
@@ -460,12 +514,12 @@ inline size_t smem_bytes2(const Params2& p, int kpad) {
            sizeof(Smem2);
 }
 
-template <int KPAD, int BIAS, bool DBG>
+template <int KPAD, int BIAS, bool DBG, bool TL = false>
 static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     static bool configured[kMaxDevices] = {};
     const int dev = current_device();
     if (!configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)kSmemMax2);
         if (e != cudaSuccess) return -(int)e;
         configured[dev] = true;
@@ -482,12 +536,13 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG>, prm, vmap, bmap);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL>, prm, vmap, bmap);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
 template <int KPAD>
 static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+    if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
     if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, stream);
     return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, stream);

@@ -38,13 +38,13 @@ bool tcgen05_supported(const ba_params* p, const char** why) {
     return w == nullptr;
 }
 
-int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, cudaStream_t stream);  // attn_tc2.cu
+int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* dbg_T, cudaStream_t stream);  // attn_tc2.cu
 
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     using namespace tc;
     // long sequences in whole 128-key tiles: the second-generation kernel (one CTA per SM, two query tiles in flight)
-    if (!g_dbg_T) {
-        const int n2 = launch_attn_tc2(a, g_dbg_S, g_dbg_head, stream);
+    {
+        const int n2 = launch_attn_tc2(a, g_dbg_S, g_dbg_head, g_dbg_T, stream);
         if (n2 != 0) return n2;
     }
     if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 16 != 0)

@@ -44,7 +44,7 @@ def timeit(tc2, Q, K, V, bias, reps=20):
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 if mode in ("all", "check"):
     for (B, H, N, d, wb) in [(1, 2, 256, 64, False), (1, 2, 256, 64, True), (2, 3, 384, 72, True), (1, 2, 512, 128, False),
-                             (1, 2, 512, 128, True), (1, 4, 1024, 72, True), (1, 2, 640, 32, False), (1, 2, 2048, 96, True)]:
+                             (1, 2, 512, 128, True), (1, 4, 1024, 72, True), (1, 2, 640, 32, False), (1, 2, 192, 64, True), (1, 3, 320, 128, False), (1, 2, 2048, 96, True)]:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
         bias = (0.5 * torch.randn(H, N, N, device="cuda")).to(torch.bfloat16) if wb else None
         scale = 1.0 / d ** 0.5
