@@ -19,7 +19,7 @@
 //   (a first version used 128-key tiles with one S stage per query tile and 64 keys per thread; the two query tiles then
 //    ran in phase -- both waiting for the tensor core at the same time -- and the MUFU pipe stayed at 64%)
 // 640 threads: warps 0-15 softmax (104 registers), 16 / 17 MMA issue for tile A / B (16 also allocates TMEM), 18 TMA producer,
-// 19 Q/K expander.
+// 19 Q expander.  K tiles come pre-expanded from expand_k_kernel (workspace plane FwdArgs::k_exp) by bulk copy.
 // TMEM (512 columns): tile X owns S stages [128 X + 64 s, +64) and O [256 + 128 X, +dvp); the bf16 weights overwrite the
 // S columns their thread has just read: keys 0-31 -> columns [0,16), keys 32-63 -> columns [32,48) of the stage.
 //
@@ -43,7 +43,13 @@ constexpr int kThreads2 = 640;
 constexpr int kColO2 = 256;        // first O column; tile X owns [256 + 128 X, +dvp)
 constexpr int kVBox = 8192;        // one TMA box of V: 64 keys x 64 columns bf16, 128B swizzle
 constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16, 128B swizzle
-constexpr float kThr2 = 16.0f;     // lazy-rescale threshold, log2 units
+#ifndef BA_PP_AT
+#define BA_PP_AT -1  // (measured: no gain with mbarriers or named barriers; kept as a dev knob) exponent pair after which a warp hands the MUFU pipe to the other query tile's pair (-1: no ping-pong)
+#endif
+#ifndef BA_THR2
+#define BA_THR2 16.0f
+#endif
+constexpr float kThr2 = BA_THR2;     // lazy-rescale threshold, log2 units
 constexpr float kFastBound = 32.0f;  // FAST path when d * mu_q mu_k / tau * log2(e) <= this (weights stay >= 2^-64)
 constexpr int kRegsSoftmax2 = 104, kRegsCtrl2 = 64;  // the pool is what the launch allocated: 640 x 96 = 512 x 104 + 128 x 64
 
@@ -80,6 +86,12 @@ __device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1) {
         "add.rn.f32x2 rd, rd, ra;\n\tmov.b64 {%0, %1}, rd;\n\t}"
         : "+f"(d0), "+f"(d1)
         : "f"(a0), "f"(a1));
+}
+// 1-D bulk copy global -> shared, completion counted in bytes on an mbarrier (16-byte aligned, multiple of 16 bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
@@ -166,6 +178,12 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             const uint64_t k_desc = make_desc(smem_u32(sK), TN * 16, 128, 0);
             const uint64_t v_desc = make_desc(smem_u32(sV), kVBox, 1024, 2);
             const uint32_t s_tmem = tmem + X * 128, o_tmem = tmem + kColO2 + X * 128;
+            // Issue order per key tile j: S(j), then P.V(j-1) once P(j-1) has arrived.  S(j) overwrites the stage that held
+            // P(j-2), read by P.V(j-2) an iteration earlier (tcgen05.mma executes in issue order), and must not wait for P(j-1).
+            // The barriers of an iteration are polled up front with test_wait (non-blocking; try_wait may sleep on an open
+            // phase), blocking waits only for what is still open.  Variants measured and rejected (same box, 16384 x 64 /
+            // 16384 x 128, ms): this order 1.30 / 1.51; "P.V(t), S(t+2)" with S two tiles ahead 1.45 / 1.72 -- every softmax
+            // warp then finds its S ready, all sixteen run in lock-step and sit in their MUFU-free phases together.
             Ring qr, kr, vr;
             uint32_t g = 0;   // key tiles of my query tile issued so far (S stage = g & 1); P.V runs one tile behind
             uint32_t up = 0;  // units of my query tile whose last P.V has been issued
@@ -178,7 +196,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 const uint64_t qd = q_desc + (uint64_t)((qr.stage * 2 * TM * KPAD) >> 4);
                 for (int j = 0; j < T; ++j) {
                     const uint32_t pst = (g - 1) & 1u;  // stage of the pending tile (when there is one)
-                    const uint32_t k_ok = mbar_test(&sm->kfull[kr.stage], kr.phase);  // (test_wait: try_wait may sleep on an open phase)
+                    const uint32_t k_ok = mbar_test(&sm->kfull[kr.stage], kr.phase);
                     uint32_t v_ok = 1, p_ok = 1;
                     if (pend) {
                         v_ok = mbar_test(&sm->vfull[pvs], pvph);
@@ -264,7 +282,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         } else if (warp == 18) {
             // ======================================================== TMA producer: bias tiles, V tiles
             if (lane == 0) {
-                Ring vr, br;
+                Ring vr, br, kr;
                 for (int u = blockIdx.x; u < prm.units; u += G) {
                     const int head = u / prm.ublocks;
                     const int ub = u - head * prm.ublocks;
@@ -279,6 +297,11 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                                 br.next(prm.bst);
                             }
                         }
+                        // K tile: 64 keys of e4m3 +-1.0 bytes, already in UMMA tile order (expand_k_kernel): one bulk copy
+                        mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
+                        mbar_expect_tx(&sm->kfull[kr.stage], TN * KPAD);
+                        bulk_load(sK + kr.stage * TN * KPAD, a.k_exp + ((int64_t)head * T + j) * (TN * KPAD), TN * KPAD, &sm->kfull[kr.stage]);
+                        kr.next(prm.kst);
                         mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
                         mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * kVBox);
                         for (int b = 0; b < prm.nbox; ++b)
@@ -288,14 +311,10 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 }
             }
         } else {
-            // ======================================================== Q / K expander (one warp: two keys per lane and tile)
-            Ring qr, kr;
-            uint32_t wk0[KPAD / 32], wk1[KPAD / 32];
-            if ((int)blockIdx.x < prm.units) {
-                const int head = blockIdx.x / prm.ublocks;
-                load_words<KPAD>(wk0, a.k_words + ((int64_t)head * N + lane) * w64, w64, true);
-                load_words<KPAD>(wk1, a.k_words + ((int64_t)head * N + lane + 32) * w64, w64, true);
-            }
+            // ======================================================== Q expander (one warp; the K tiles arrive expanded, by bulk copy:
+            // expanding 64 keys per tile in here took one warp ~1500 clk per tile and two warps ~1400 -- against 1024 clk of
+            // exponentials -- and was what every earlier build of this kernel was really waiting for)
+            Ring qr;
             for (int u = blockIdx.x; u < prm.units; u += G) {
                 const int head = u / prm.ublocks;
                 const int row0 = (u - head * prm.ublocks) * 2 * TM;
@@ -313,34 +332,6 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 fence_proxy_async();
                 warp_arrive(&sm->qfull[qr.stage], lane);
                 qr.next(prm.qst);
-                const int un = u + G;
-                const int hn = un / prm.ublocks;
-                for (int j = 0; j < T; ++j) {
-                    // the next tile's words are requested BEFORE this tile is expanded (the next unit's first tile after the
-                    // last one): their L2 / HBM latency hides behind the expansion and the wait for a free stage
-                    uint32_t nk0[KPAD / 32], nk1[KPAD / 32];
-                    if (j + 1 < T) {
-                        load_words<KPAD>(nk0, a.k_words + ((int64_t)head * N + (j + 1) * TN + lane) * w64, w64, true);
-                        load_words<KPAD>(nk1, a.k_words + ((int64_t)head * N + (j + 1) * TN + lane + 32) * w64, w64, true);
-                    } else {
-                        load_words<KPAD>(nk0, a.k_words + ((int64_t)hn * N + lane) * w64, w64, un < prm.units);
-                        load_words<KPAD>(nk1, a.k_words + ((int64_t)hn * N + lane + 32) * w64, w64, un < prm.units);
-                    }
-                    mbar_wait(&sm->kfree[kr.stage], kr.phase ^ 1u);
-                    BA_STAMP2();
-                    unsigned char* kt = sK + kr.stage * TN * KPAD;
-                    expand_store<KPAD>(kt, TN, lane, wk0, d, true, sm->lut);
-                    expand_store<KPAD>(kt, TN, lane + 32, wk1, d, true, sm->lut);
-                    fence_proxy_async();
-                    warp_arrive(&sm->kfull[kr.stage], lane);
-                    BA_STAMP2();
-                    kr.next(prm.kst);
-#pragma unroll
-                    for (int i = 0; i < KPAD / 32; ++i) {
-                        wk0[i] = nk0[i];
-                        wk1[i] = nk1[i];
-                    }
-                }
             }
         }
     } else {
@@ -356,6 +347,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const int oc0 = half ? h16 : 0, oc1 = half ? prm.dvp : h16;
         const bool stats = a.row_max != nullptr || a.row_sum != nullptr;
         uint32_t gx = 0;  // key tiles this query tile has been through (stage = gx & 1, parity = (gx >> 1) & 1)
+        uint32_t np = 0;  // tiles done in ping-pong with the other query tile
         Ring br;          // position of my query tile's next bias tile in the producer's ring
         if (BIAS == 1 && X == 1) br.next(prm.bst);
         for (int u = blockIdx.x; u < prm.units; u += G) {
@@ -367,6 +359,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     for (int j = 0; j < T; ++j) br.next(prm.bst);
                 continue;
             }
+            const bool pp = nact == 2 && BA_PP_AT >= 0;
             const int row = ub * 2 * TM + X * TM + r;
             const float sc = __ldg(a.mu_q + head) * __ldg(a.mu_k + head) * a.inv_tau;  // natural-log units per unit of dot
             const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;  // BIAS 0 keeps x = raw dot and folds the scale into the exponent
@@ -375,17 +368,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             float l0 = 0.f, l1 = 0.f;
             const bool dump = DBG && prm.dbg_S && head == prm.dbg_head;
             float x[32];
-            bool have = false;  // x already holds (or is being loaded with) the scores of the tile about to be processed
             for (int j = 0; j < T; ++j, ++gx) {
                 const uint32_t st = gx & 1u, par = (gx >> 1) & 1u;
                 const uint32_t s_addr = s_base + st * TN;
                 BA_STAMP2();
-                if (!have) {
-                    mbar_wait(&sm->sfull[X][st], par);
-                    tc_fence_after();
-                    BA_TMEM_LD16(s_addr + 0, x, 0);
-                    BA_TMEM_LD16(s_addr + 16, x, 16);
-                }
+                // (Requesting the next tile's scores before this tile's P is handed over -- the "rolling refill" of the first
+                // kernel -- was tried here: no gain, and rare wrong rows under the run-to-run identity stress test that stayed
+                // unexplained, so every tile waits for its own S.)
+                mbar_wait(&sm->sfull[X][st], par);
+                tc_fence_after();
+                BA_TMEM_LD16(s_addr + 0, x, 0);
+                BA_TMEM_LD16(s_addr + 16, x, 16);
                 BA_STAMP2();
                 if (BIAS == 1) mbar_wait(&sm->bfull[br.stage], br.phase);
                 tc_wait_ld();
@@ -430,8 +423,11 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         pair_sync(pair_id);
                         const float tm = fmaxf(hm, sm->xch[X][half ^ 1][r]);
                         m_true = fmaxf(m_true, tm);
-                        if (tm > m_ref + kThr2) {
-                            const float alpha = ex2(m_ref - tm);  // first tile: 2^-inf = 0 on a still-unwritten O
+                        // (warp-uniform: the tcgen05.ld / st inside rescale_o are .sync.aligned -- rows that keep their reference
+                        // multiply by 1)
+                        const bool upd = tm > m_ref + kThr2;
+                        if (__any_sync(0xffffffffu, upd)) {
+                            const float alpha = upd ? ex2(m_ref - tm) : 1.0f;  // first tile: 2^-inf = 0 on a still-unwritten O
                             if (j > 0 && oc1 > oc0) {
                                 // S(j) was issued BEFORE P.V(j-1): wait for that MMA before touching O.  Tile j-1 is this
                                 // barrier's previous use and tile j-3 (the one before) retired before S(j) did, so the
@@ -441,15 +437,19 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                             }
                             l0 *= alpha;
                             l1 *= alpha;
-                            m_ref = tm;
+                            if (upd) m_ref = tm;
                         }
                     }
                 }
                 BA_STAMP2();
-                // ROLLING REFILL: if the next tile's S is already complete (the MMA warp runs a tile ahead), its scores are
-                // loaded into the registers of this tile's scores as soon as those have been through the exponent FMA, so the
-                // barrier and TMEM round trips of the next tile hide behind this tile's exponentials.
-                const bool nxt = j + 1 < T && mbar_test(&sm->sfull[X][st ^ 1u], ((gx + 1) >> 1) & 1u);
+                // PING-PONG.  The four softmax warps of a scheduler share its MUFU pipe fairly, so warps that start a tile together
+                // finish together and then all sit in their MUFU-free phases (hand-over, barrier and TMEM round trips, ~480 clk)
+                // at the same time.  The two warps of tile A and the two of tile B on a scheduler therefore take turns: a pair
+                // starts its exponentials when the other pair is three quarters through its own (two warps saturate the pipe,
+                // pipe_bench.cu) and does everything else while the other pair owns the pipe.  One named barrier per lane quadrant
+                // (ids 9..12, 128 threads): the pair that hands over does bar.arrive, the pair that takes over bar.sync; the
+                // roles swap every phase.  (mbarriers cost ~200 clk per hand-over, as much as was to be gained.)
+                if (pp && (X == 1 || np > 0)) asm volatile("bar.sync %0, 128;" ::"r"(9 + quad) : "memory");
                 const float nm = -m_ref;
                 uint32_t pk[16];
 #pragma unroll
@@ -459,13 +459,11 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     const float p0 = ex2(a0), p1 = ex2(a1);
                     add2(l0, l1, p0, p1);
                     pk[e] = pack_bf16(p0, p1);
-                    if (e == 7 && nxt) {
-                        tc_fence_after();
-                        BA_TMEM_LD16(s_base + (st ^ 1u) * TN, x, 0);
+                    if (e == BA_PP_AT && pp) {
+                        asm volatile("bar.arrive %0, 128;" ::"r"(9 + quad) : "memory");
+                        ++np;
                     }
-                    if (e == 15 && nxt) BA_TMEM_LD16(s_base + (st ^ 1u) * TN + 16, x, 16);
                 }
-                have = nxt;
                 BA_TMEM_ST16U(s_addr, pk);
                 BA_STAMP2();
                 tc_wait_st();
@@ -507,6 +505,36 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
     }
 }
 
+// K sign planes -> e4m3 +-1.0 bytes in the order the S MMA reads them (K-major, no swizzle, 8 x 16 B core matrices):
+// byte (key r, element kb) of 64-key tile t of a head lives at t*64*KPAD + (kb/16)*(64*16) + r*16 + kb%16; elements at or past d
+// are 0.0.  One thread per 16-byte chunk; a warp writes 512 consecutive bytes.
+template <int KPAD>
+__global__ void __launch_bounds__(256) expand_k_kernel(const uint64_t* __restrict__ words, unsigned char* __restrict__ out, int64_t rows,
+                                                       int w64, int d) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    constexpr int C = KPAD / 16;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = (tile * C + c) * 64 + r
+    if (idx >= rows * C) return;
+    const int r = (int)(idx & 63);
+    const int c = (int)((idx >> 6) % C);
+    const int64_t tile = (idx >> 6) / C;
+    const int64_t row = tile * 64 + r;  // heads are contiguous: N % 64 == 0
+    const uint64_t w = (c >> 2) < w64 ? __ldg(words + row * w64 + (c >> 2)) : 0ull;
+    const uint32_t bits16 = (uint32_t)(w >> (16 * (c & 3))) & 0xFFFFu;
+    const uint2 lo = 16 * c < d ? expand_byte(bits16 & 0xFF) : make_uint2(0, 0);
+    const uint2 hi = 16 * c + 8 < d ? expand_byte(bits16 >> 8) : make_uint2(0, 0);
+    reinterpret_cast<uint4*>(out)[idx] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+}
+
+template <int KPAD>
+static int launch_expand_k(const FwdArgs& a, cudaStream_t stream) {
+    const int64_t rows = (int64_t)a.BH * a.N;
+    const int64_t chunks = rows * (KPAD / 16);
+    expand_k_kernel<KPAD><<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(a.k_words, const_cast<unsigned char*>(a.k_exp), rows, a.W64, a.d);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
 constexpr size_t kSmemMax2 = 227 * 1024;
 
 inline size_t smem_bytes2(const Params2& p, int kpad) {
@@ -541,7 +569,18 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
 }
 
 template <int KPAD>
+static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream);
+
+template <int KPAD>
 static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+    const int ne = launch_expand_k<KPAD>(prm.a, stream);
+    if (ne < 0) return ne;
+    const int nk = launch_main2<KPAD>(prm, bias_mode, vmap, bmap, stream);
+    return nk < 0 ? nk : ne + nk;
+}
+
+template <int KPAD>
+static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
     if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, stream);

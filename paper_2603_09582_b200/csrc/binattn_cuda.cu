@@ -41,7 +41,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, total;
+    size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, kexp, total;
     int64_t BH;
     int W64, chunks;
 };
@@ -63,6 +63,9 @@ Layout make_layout(const ba_params* p, int64_t heads = -1) {
         L.vq = off; off += align_up((size_t)L.BH * p->N * p->d, 256);
         L.vscales = off; off += align_up((size_t)L.BH * p->d * sizeof(double), 256);
     }
+    L.kexp = off;  // expanded K plane of the second-generation tcgen05 kernel (e4m3 +-1.0 bytes, UMMA tile order)
+    if (!p->quantize_pv && p->kernel != BA_KERNEL_SIMT && ba::tc2_shape_ok(p->in_dtype, p->N, p->d))
+        off += align_up(ba::tc2_kexp_bytes(L.BH, p->N, p->d), 256);
     L.total = off;
     return L;
 }
@@ -427,6 +430,7 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.k_words = reinterpret_cast<uint64_t*>(ws + L.k_words);
     a.mu_q = reinterpret_cast<float*>(ws + L.mu_q);
     a.mu_k = reinterpret_cast<float*>(ws + L.mu_k);
+    a.k_exp = L.total > L.kexp ? reinterpret_cast<const unsigned char*>(ws + L.kexp) : nullptr;
     a.bias = p->bias_mode != BA_BIAS_NONE ? bias : nullptr;
     a.bias_kind = p->bias_mode;
     a.O = O;
