@@ -16,6 +16,8 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     using namespace tc2;
     if (env_long("BA_TC2", 1) == 0) return 0;
     if (!tc2_shape_ok(a.in_dtype, a.N, a.d) || !a.k_exp) return 0;
+    if (a.N < env_long("BA_TC2_MIN_N", 0)) return 0;  // dev knob
+    if (dbg_S && a.N % TN != 0) return 0;  // (the logits dump has no ragged instantiation)
     if (a.d % 8 != 0 || a.d > 128) return 0;
     if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 32 != 0) return 0;
     int bias_mode = 0;
@@ -29,7 +31,7 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     if (!enc) return 0;
     Params2 prm{};
     prm.a = a;
-    prm.tiles = a.N / TN;
+    prm.tiles = (a.N + TN - 1) / TN;
     prm.ublocks = (a.N + 2 * TM - 1) / (2 * TM);
     prm.units = a.BH * prm.ublocks;
     prm.dvp = (a.d + 15) / 16 * 16;

@@ -95,13 +95,14 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-// BIAS: 0 = none, 1 = dense bf16 table staged by TMA.  N % 64 == 0.
+// BIAS: 0 = none, 1 = dense bf16 table staged by TMA.  Any N >= 128: the K plane is zero-padded to whole 64-key tiles, V and bias
+// tiles are zero-filled past N by the TMA unit, and the last tile's surplus columns are masked to -inf before the row max.
 #define BA_STAMP2()                                                      \
     do {                                                                 \
         if (TL && tl_buf && tl_n < kTlStamps) tl_buf[tl_n++] = clock64(); \
     } while (0)
 
-template <int KPAD, int BIAS, bool DBG, bool TL = false>
+template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
 __global__ void __launch_bounds__(kThreads2, 1)
 attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUtensorMap vmap,
                 const __grid_constant__ CUtensorMap bmap) {
@@ -346,6 +347,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const int h16 = ((prm.dvp >> 1) + 15) & ~15;             // O columns [0,h16) belong to half 0, [h16,dvp) to half 1
         const int oc0 = half ? h16 : 0, oc1 = half ? prm.dvp : h16;
         const bool stats = a.row_max != nullptr || a.row_sum != nullptr;
+        const int nlast = N - (T - 1) * TN;  // keys of the last tile (TN unless N is ragged)
         uint32_t gx = 0;  // key tiles this query tile has been through (stage = gx & 1, parity = (gx >> 1) & 1)
         uint32_t np = 0;  // tiles done in ping-pong with the other query tile
         Ring br;          // position of my query tile's next bias tile in the producer's ring
@@ -386,7 +388,8 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 if (DBG && dump) {
                     int32_t* drow = prm.dbg_S + (int64_t)row * N + j * TN + half * 32;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) drow[i] = (int)x[i];
+                    for (int i = 0; i < 32; ++i)
+                        if (row < N && j * TN + half * 32 + i < N) drow[i] = (int)x[i];
                 }
                 if (BIAS == 1) {
                     const unsigned char* brow = sB + br.stage * kBSub + r * 128;  // row r of the 128 x 64 bf16 tile
@@ -402,6 +405,12 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     warp_arrive(&sm->bfree[br.stage], lane);
                     br.next(prm.bst);  // tile A and tile B alternate in the ring when both are active
                     if (nact == 2) br.next(prm.bst);
+                }
+                if (RAGGED && j == T - 1) {  // ragged N (its own instantiation: the test and the masking loop cost the others 5-13%): keys at or past N get weight 0 (attention.cpp:285-287 stops the block there)
+                    const int nk = nlast - half * 32;  // valid keys among my 32 columns
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i >= nk) x[i] = -INFINITY;
                 }
                 if (!fast) {
                     float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
@@ -509,28 +518,30 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
 // byte (key r, element kb) of 64-key tile t of a head lives at t*64*KPAD + (kb/16)*(64*16) + r*16 + kb%16; elements at or past d
 // are 0.0.  One thread per 16-byte chunk; a warp writes 512 consecutive bytes.
 template <int KPAD>
-__global__ void __launch_bounds__(256) expand_k_kernel(const uint64_t* __restrict__ words, unsigned char* __restrict__ out, int64_t rows,
-                                                       int w64, int d) {
+__global__ void __launch_bounds__(256) expand_k_kernel(const uint64_t* __restrict__ words, unsigned char* __restrict__ out, int64_t heads,
+                                                       int N, int tiles, int w64, int d) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int C = KPAD / 16;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = (tile * C + c) * 64 + r
-    if (idx >= rows * C) return;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = ((head * tiles + tile) * C + c) * 64 + r
+    if (idx >= heads * tiles * C * 64) return;
     const int r = (int)(idx & 63);
     const int c = (int)((idx >> 6) % C);
-    const int64_t tile = (idx >> 6) / C;
-    const int64_t row = tile * 64 + r;  // heads are contiguous: N % 64 == 0
-    const uint64_t w = (c >> 2) < w64 ? __ldg(words + row * w64 + (c >> 2)) : 0ull;
+    const int64_t ht = (idx >> 6) / C;  // head * tiles + tile
+    const int64_t head = ht / tiles;
+    const int key = (int)(ht - head * tiles) * 64 + r;  // keys at or past N (last tile of a ragged head) expand to zeros
+    const bool valid = key < N;
+    const uint64_t w = (valid && (c >> 2) < w64) ? __ldg(words + (head * N + key) * w64 + (c >> 2)) : 0ull;
     const uint32_t bits16 = (uint32_t)(w >> (16 * (c & 3))) & 0xFFFFu;
-    const uint2 lo = 16 * c < d ? expand_byte(bits16 & 0xFF) : make_uint2(0, 0);
-    const uint2 hi = 16 * c + 8 < d ? expand_byte(bits16 >> 8) : make_uint2(0, 0);
+    const uint2 lo = (valid && 16 * c < d) ? expand_byte(bits16 & 0xFF) : make_uint2(0, 0);
+    const uint2 hi = (valid && 16 * c + 8 < d) ? expand_byte(bits16 >> 8) : make_uint2(0, 0);
     reinterpret_cast<uint4*>(out)[idx] = make_uint4(lo.x, lo.y, hi.x, hi.y);
 }
 
 template <int KPAD>
-static int launch_expand_k(const FwdArgs& a, cudaStream_t stream) {
-    const int64_t rows = (int64_t)a.BH * a.N;
-    const int64_t chunks = rows * (KPAD / 16);
-    expand_k_kernel<KPAD><<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(a.k_words, const_cast<unsigned char*>(a.k_exp), rows, a.W64, a.d);
+static int launch_expand_k(const FwdArgs& a, int tiles, cudaStream_t stream) {
+    const int64_t chunks = (int64_t)a.BH * tiles * (KPAD / 16) * 64;
+    expand_k_kernel<KPAD><<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(a.k_words, const_cast<unsigned char*>(a.k_exp), a.BH, a.N, tiles,
+                                                                              a.W64, a.d);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
@@ -542,12 +553,12 @@ inline size_t smem_bytes2(const Params2& p, int kpad) {
            sizeof(Smem2);
 }
 
-template <int KPAD, int BIAS, bool DBG, bool TL = false>
+template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
 static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     static bool configured[kMaxDevices] = {};
     const int dev = current_device();
     if (!configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)kSmemMax2);
         if (e != cudaSuccess) return -(int)e;
         configured[dev] = true;
@@ -564,7 +575,7 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL>, prm, vmap, bmap);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, prm, vmap, bmap);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
@@ -573,7 +584,7 @@ static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vm
 
 template <int KPAD>
 static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
-    const int ne = launch_expand_k<KPAD>(prm.a, stream);
+    const int ne = launch_expand_k<KPAD>(prm.a, prm.tiles, stream);
     if (ne < 0) return ne;
     const int nk = launch_main2<KPAD>(prm, bias_mode, vmap, bmap, stream);
     return nk < 0 ? nk : ne + nk;
@@ -583,6 +594,10 @@ template <int KPAD>
 static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
+    if (prm.a.N % TN != 0) {
+        if (bias_mode == 1) return launch_variant2<KPAD, 1, false, false, true>(prm, vmap, bmap, stream);
+        return launch_variant2<KPAD, 0, false, false, true>(prm, vmap, bmap, stream);
+    }
     if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, stream);
     return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, stream);
 }

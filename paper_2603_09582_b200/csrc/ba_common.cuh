@@ -20,7 +20,7 @@ struct FwdArgs {
     const uint64_t* k_words;  // [BH, N, W64]
     const float* mu_q;        // [BH]
     const float* mu_k;        // [BH]
-    const unsigned char* k_exp;  // [BH, N/64, KPAD/16, 64, 16] e4m3 +-1.0 bytes of K in UMMA tile order (second-generation
+    const unsigned char* k_exp;  // [BH, ceil(N/64), KPAD/16, 64, 16] e4m3 +-1.0 bytes of K in UMMA tile order (second-generation
                                  // tcgen05 kernel only; nullptr when the workspace has no room for it)
     const void* bias;         // dense: [bias_heads, N, bias_ld]; rel1d: [bias_heads, 2N-1]; or nullptr
     int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D
@@ -49,9 +49,11 @@ int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, i
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
 // Shapes the second-generation tcgen05 kernel (attn_tc2.cuh) takes; decides whether the workspace carries the expanded K plane.
 inline bool tc2_shape_ok(int in_dtype, int N, int d) {
-    return in_dtype == BA_BF16 && d % 8 == 0 && d <= 128 && N % 64 == 0 && N >= 128;
+    return in_dtype == BA_BF16 && d % 8 == 0 && d <= 128 && N >= 512;  // below ~512 keys the first-generation kernel is faster (measured)
 }
-inline size_t tc2_kexp_bytes(int64_t heads, int N, int d) { return (size_t)heads * N * ((d + 31) / 32 * 32); }
+inline size_t tc2_kexp_bytes(int64_t heads, int N, int d) {  // whole 64-key tiles per head
+    return (size_t)heads * ((N + 63) / 64 * 64) * ((d + 31) / 32 * 32);
+}
 // diagnostics (fidelity.cu)
 int launch_head_mean_abs(const void* Q, const void* K, int dtype, int64_t count, double* mu, cudaStream_t stream);
 int launch_probs_rows(const void* Q, const void* K, const void* bias, const int32_t* rows, int nrows, const double* mu, double* P,

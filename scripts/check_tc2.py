@@ -44,9 +44,10 @@ def timeit(tc2, Q, K, V, bias, reps=20):
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 if mode in ("all", "check"):
     for (B, H, N, d, wb) in [(1, 2, 256, 64, False), (1, 2, 256, 64, True), (2, 3, 384, 72, True), (1, 2, 512, 128, False),
-                             (1, 2, 512, 128, True), (1, 4, 1024, 72, True), (1, 2, 640, 32, False), (1, 2, 192, 64, True), (1, 3, 320, 128, False), (1, 2, 2048, 96, True)]:
+                             (1, 2, 512, 128, True), (1, 4, 1024, 72, True), (1, 2, 640, 32, False), (1, 2, 192, 64, True), (1, 3, 320, 128, False), (1, 2, 2048, 96, True),
+                             (1, 6, 577, 64, True), (1, 6, 513, 64, False), (2, 3, 700, 72, True), (1, 2, 833, 128, False), (1, 2, 1000, 96, True), (2, 2, 1023, 64, True), (1, 2, 639, 32, False)]:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
-        bias = (0.5 * torch.randn(H, N, N, device="cuda")).to(torch.bfloat16) if wb else None
+        bias = (0.5 * torch.randn(H, N, (N + 7) // 8 * 8, device="cuda")).to(torch.bfloat16)[:, :, :N] if wb else None
         scale = 1.0 / d ** 0.5
         ref = ref64(Q, K, V, bias, scale)
         o1 = run(False, Q, K, V, bias)
@@ -61,7 +62,7 @@ if mode in ("all", "time"):
                          (1, 16, 16384, 128), (32, 16, 1024, 72)]:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
         for wb in (False, True):
-            bias = (0.5 * torch.randn(H, N, N, device="cuda")).to(torch.bfloat16) if wb else None
+            bias = (0.5 * torch.randn(H, N, (N + 7) // 8 * 8, device="cuda")).to(torch.bfloat16)[:, :, :N] if wb else None
             t1 = timeit(False, Q, K, V, bias, 10)
             t2 = timeit(True, Q, K, V, bias, 10)
             tops = 4.0 * B * H * N * N * d / (t2 * 1e-3) / 1e12
