@@ -426,13 +426,16 @@ def test_large_logit_scale_rescale_path(ba, port):
     """Inputs scaled by 16 make mu_q*mu_k/tau ~ 20 per unit of dot: row maxima move by far more than the lazy-rescale
     threshold from tile to tile, so the O/l rescale branch runs for real; the result must still match the oracle.
     In this regime a row's weight sits on two or three tied keys, so the 2^-9 rounding of each bf16 weight no longer
-    averages out: the tensor-core path is held to 3 * 2^-9 * max|V| (~6e-3 * 1) instead of the typical-input bar."""
+    averages out: the tensor-core path is held to its guaranteed bound 2^-8 * max|V| (each bf16 weight is within 2^-9
+    relative of exp(S - m), so |dO| <= 2^-9 * max_j |v_j - O| <= 2^-8 * max|V|; stated in include/binattn_cuda.h with a
+    measured error-vs-peakedness table in INTEGRATION.md) instead of the typical-input bar."""
     n, d = 300, 64
     heads = []
     for s in range(2):
         q, k, v, b = make_head_inputs(port, 22, s, n, d, bias_scale=0.5)
         heads.append((q * 16.0, k * 16.0, v, b))  # power of two: still exactly representable in bf16
-    run_and_compare(ba, port, heads, n, d, "bf16", "per_head", tol={"tcgen05": 6e-3})
+    bound = 2.0 ** -8 * max(float(np.abs(h[2]).max()) for h in heads)
+    run_and_compare(ba, port, heads, n, d, "bf16", "per_head", tol={"tcgen05": bound})
 
 
 def test_error_codes_on_device(ba):
