@@ -50,14 +50,21 @@ typedef enum {
 typedef enum {
     BA_BIAS_NONE = 0,
     BA_BIAS_DENSE = 1,  /* DenseBias: N x N table (attention.hpp:15-17, attention.cpp:59-63) */
-    BA_BIAS_REL1D = 2   /* Relative1dBias: b_ij = offsets[i - j + N - 1], 2N-1 entries per table (attention.hpp:18-21,
+    BA_BIAS_REL1D = 2,  /* Relative1dBias: b_ij = offsets[i - j + N - 1], 2N-1 entries per table (attention.hpp:18-21,
                            attention.cpp:65-76); generated inside the kernel, no N x N table ever exists */
+    BA_BIAS_REL2D = 3   /* Relative2dBias: tokens on a g x g grid, g = sqrt(N) (N must be a perfect square, else BA_ERR_SHAPE
+                           like attention.cpp:79-81), b_ij = row_offsets[ri - rj + g - 1] + col_offsets[ci - cj + g - 1]
+                           (attention.hpp:22-26, attention.cpp:78-96).  Generated inside the kernel from the two tables
+                           held in shared memory when the second-generation tcgen05 kernel takes the shape (N >= 512,
+                           g % 32 == 0: N = 1024, 4096, 16384); otherwise expanded ONCE on the device into a handle-owned
+                           fp32 table and fed to the dense path */
 } ba_bias_mode;
 
 /* Q, K, V: [B, H, N, d] row-major contiguous, dtype in_dtype.  O: [B, H, N, d] float32.
  * bias (bias_mode == BA_BIAS_DENSE): [bias_heads, N, bias_ld] with bias_heads in {1, H}; head (b,h)
  * reads table h % bias_heads; bias_ld >= N is the row stride in elements (0 means N).
- * bias (bias_mode == BA_BIAS_REL1D): [bias_heads, 2N-1] contiguous offsets (bias_ld is ignored). */
+ * bias (bias_mode == BA_BIAS_REL1D): [bias_heads, 2N-1] contiguous offsets (bias_ld is ignored).
+ * bias (bias_mode == BA_BIAS_REL2D): [bias_heads, 2, 2g-1] contiguous: row_offsets then col_offsets of each table (bias_ld ignored). */
 typedef struct {
     int32_t B, H, N, d;
     int32_t in_dtype;    /* ba_dtype of Q, K, V */

@@ -125,7 +125,9 @@ class Relative1dBias:
 class Relative2dBias:
     """binattn::Relative2dBias (attention.hpp:22-26): N = g*g tokens on a g x g grid,
     b_ij = row_offsets[ri - rj + g - 1] + col_offsets[ci - cj + g - 1], both tables of length 2g-1 (or [1|H, 2g-1]).
-    Expanded on the device to the dense table materialize_bias builds (attention.cpp:78-96) and fed to the dense path."""
+    Passed to the C ABI as BA_BIAS_REL2D: generated inside the second-generation tcgen05 kernel from the two tables (N >= 512,
+    g % 32 == 0), else expanded once on the device to the table materialize_bias builds (attention.cpp:78-96).
+    `materialize` is that table, for tests and for callers of the dense path."""
     row_offsets: torch.Tensor
     col_offsets: torch.Tensor
 
@@ -150,7 +152,11 @@ class AttentionConfig:
     """binattn::AttentionConfig (attention.hpp:29-41).  block_rows/block_cols are accepted and validated like the
     reference's (attention.cpp:26-28) but do not change the result: the CUDA kernels pick their own tiles and the
     reference itself is tile-invariant to 1e-12 (test_attention.cpp:254-272).  quantize_pv=True runs the integer P.V
-    mode on the CUDA cores, where block_cols (<= 64) DOES shape the result, exactly as in the reference."""
+    mode on the CUDA cores, where block_cols (<= 64) DOES shape the result, exactly as in the reference.
+
+    DELIBERATE DEVIATION: quantize_pv defaults to False here, to True in the reference (attention.hpp:35).  False is the
+    fp P.V mode the tensor-core product path implements and O-parity is defined against; set
+    quantize_pv=True to get the reference's default arithmetic when porting `AttentionConfig::make(n, d)`."""
     seq_len: int = 0
     head_dim: int = 0
     temperature: float = 1.0
@@ -203,7 +209,12 @@ class BinaryAttention:
         p = _Params(B=B, H=H, N=N, d=d, in_dtype=_DTYPES[dtype], kernel=KERNELS[kernel])
         p.quantize_pv, p.block_cols = int(bool(quantize_pv)), int(block_cols or 0)
         p.inv_tau = (1.0 / math.sqrt(d)) if scale is None else float(scale)
-        if isinstance(bias, Relative1dBias):
+        if isinstance(bias, Relative2dBias):
+            tb = bias.row_offsets  # (_check_bias packed both tables into one [Hb, 2, 2g-1] tensor and stored it here)
+            if tb.dtype not in (torch.bfloat16, torch.float32):
+                raise ValidationError("bias must be bfloat16 or float32")
+            p.bias_mode, p.bias_heads, p.bias_dtype, p.bias_ld = 3, tb.shape[0], _DTYPES[tb.dtype], 0
+        elif isinstance(bias, Relative1dBias):
             off = bias.offsets
             if off.dtype not in (torch.bfloat16, torch.float32):
                 raise ValidationError("bias must be bfloat16 or float32")
@@ -221,7 +232,16 @@ class BinaryAttention:
         if bias is None:
             return None, None
         if isinstance(bias, Relative2dBias):
-            bias = bias.materialize(N)
+            g = int(round(math.sqrt(N)))
+            if g * g != N:
+                raise ShapeError("bias: relative-2d requires N to be a perfect square")  # attention.cpp:79-81
+            ro, co = bias.row_offsets, bias.col_offsets
+            ro = ro.unsqueeze(0) if ro.dim() == 1 else ro
+            co = co.unsqueeze(0) if co.dim() == 1 else co
+            if ro.dim() != 2 or co.shape != ro.shape or ro.shape[1] != 2 * g - 1 or ro.shape[0] not in (1, H):
+                raise ShapeError("bias: relative-2d tables must have length 2*sqrt(N)-1")  # attention.cpp:82-83
+            packed = torch.stack([ro, co.to(ro.dtype)], dim=1).contiguous()  # [Hb, 2, 2g-1]
+            return Relative2dBias(packed, packed), packed
         if isinstance(bias, Relative1dBias):
             off = bias.offsets
             if off.dim() == 1:
@@ -356,7 +376,7 @@ class BinaryAttention:
         B, H, N, d = Q.shape
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
         bias, bias_t = self._check_bias(bias, H, N)
-        if bias_t is not None and not isinstance(bias, Relative1dBias):
+        if bias_t is not None and not isinstance(bias, (Relative1dBias, Relative2dBias)):
             bias = bias_t = bias_t.contiguous()
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
         if out is None:

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbinattn_cuda.so")
-SOURCES = ["binattn_cuda.cu", "pack_signs.cu", "binary_logits.cu", "attn_simt.cu", "attn_int8.cu", "fidelity.cu", "attn_tcgen05.cu", "attn_tc2.cu",
+SOURCES = ["binattn_cuda.cu", "pack_signs.cu", "binary_logits.cu", "attn_simt.cu", "attn_int8.cu", "fidelity.cu", "bias_expand.cu", "attn_tcgen05.cu", "attn_tc2.cu",
            "attn_tcgen05_k32.cu", "attn_tcgen05_k64.cu", "attn_tcgen05_k96.cu", "attn_tcgen05_k128.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -1,4 +1,6 @@
 // attn_tc2.cu -- host side of the second-generation K2 (attn_tc2.cuh): shape gate, ring depths, tensor maps, dispatch.
+#include <cmath>
+
 #include "attn_tc2.cuh"
 
 namespace ba {
@@ -21,7 +23,12 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     if (a.d % 8 != 0 || a.d > 128) return 0;
     if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 32 != 0) return 0;
     int bias_mode = 0;
-    if (a.bias) {
+    int g = 0;
+    if (a.bias && a.bias_kind == BA_BIAS_REL2D) {
+        g = (int)std::lround(std::sqrt((double)a.N));
+        if ((long long)g * g != a.N || g % 32 != 0 || g > 128) return 0;  // (the C-ABI layer expands the table for these)
+        bias_mode = 4;
+    } else if (a.bias) {
         if (a.bias_kind != BA_BIAS_DENSE) return 0;
         const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 && reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         if (!tma_ok) return 0;
@@ -38,13 +45,14 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     prm.nbox = (a.d + 63) / 64;
     prm.dbg_S = dbg_S;
     prm.dbg_head = dbg_head;
+    prm.g = g;
     prm.dbg_T = dbg_T;
     const int kpad = (a.d + 31) / 32 * 32;
     // ring depths: as deep as 227 KB allow; the bias ring must cover the HBM latency of the N x N stream
     prm.kst = 4;
     prm.vst = 4;
     prm.qst = 2;
-    prm.bst = bias_mode ? 6 : 0;
+    prm.bst = bias_mode == 1 ? 6 : 0;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.kst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 5) prm.bst = 5;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.qst = 1;

@@ -65,6 +65,7 @@ struct Smem2 {
     uint2 lut[256];               // byte of sign bits -> 8 e4m3 +-1.0 bytes
     float xch[2][2][TM];          // (query tile, column half, row): half-row max / partial denominator for the other half
     uint32_t flag[2][2][4][2];    // (tile parity, query tile, lane quadrant, column half): "my warp needs a new reference max"
+    float rel2[3][2][256];        // BIAS 4: row / col offset tables (2g-1 <= 255 entries) of the heads of three consecutive units
     uint32_t tmem_base;
 };
 
@@ -76,6 +77,7 @@ struct Params2 {
     int dvp;       // d rounded up to 16
     int nbox;      // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;
+    int g;         // BIAS 4: grid side sqrt(N) (a multiple of 32)
     int32_t* dbg_S;
     int dbg_head;
     long long* dbg_T;
@@ -95,7 +97,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-// BIAS: 0 = none, 1 = dense bf16 table staged by TMA.  Any N >= 128: the K plane is zero-padded to whole 64-key tiles, V and bias
+// BIAS: 0 = none, 1 = dense bf16 table staged by TMA, 4 = Relative2dBias generated from its two offset tables (see below).  Any N >= 128: the K plane is zero-padded to whole 64-key tiles, V and bias
 // tiles are zero-filled past N by the TMA unit, and the last tile's surplus columns are masked to -inf before the row max.
 #define BA_STAMP2()                                                      \
     do {                                                                 \
@@ -316,10 +318,22 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             // expanding 64 keys per tile in here took one warp ~1500 clk per tile and two warps ~1400 -- against 1024 clk of
             // exponentials -- and was what every earlier build of this kernel was really waiting for)
             Ring qr;
-            for (int u = blockIdx.x; u < prm.units; u += G) {
+            int ui = 0;  // units of this CTA so far
+            for (int u = blockIdx.x; u < prm.units; u += G, ++ui) {
                 const int head = u / prm.ublocks;
                 const int row0 = (u - head * prm.ublocks) * 2 * TM;
                 mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
+                if (BIAS == 4) {
+                    // Relative2dBias tables of the unit's head (attention.hpp:22-26), published with the Q stage: the softmax
+                    // warps read them after the first S of the unit (qfull -> MMA -> sfull orders the accesses).  Three slots:
+                    // slot ui % 3 is rewritten for unit ui + 3, i.e. after every S MMA of unit ui + 1 has retired (qfree), by
+                    // which time the softmax warps have long left unit ui (its last P precedes the next unit's third S).
+                    const int len = 2 * prm.g - 1;
+                    const int bh = (a.head0 + head) % a.H % a.bias_heads;
+                    const char* tb = static_cast<const char*>(a.bias) + (size_t)bh * 2 * len * dtype_size(a.bias_dtype);
+                    float* dst = &sm->rel2[ui % 3][0][0];
+                    for (int i = lane; i < 2 * len; i += 32) dst[(i >= len ? 256 - len : 0) + i] = load_as_float(tb, a.bias_dtype, i);
+                }
                 unsigned char* qt = sQ + qr.stage * 2 * TM * KPAD;
 #pragma unroll 1
                 for (int i = 0; i < 8; i += 2) {  // the unit's 256 query rows, two per lane and pass (rows past N expand to zeros)
@@ -349,6 +363,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const bool stats = a.row_max != nullptr || a.row_sum != nullptr;
         const int nlast = N - (T - 1) * TN;  // keys of the last tile (TN unless N is ragged)
         uint32_t gx = 0;  // key tiles this query tile has been through (stage = gx & 1, parity = (gx >> 1) & 1)
+        int usm = -1;     // units of this CTA so far (slot of the BIAS 4 tables)
         uint32_t np = 0;  // tiles done in ping-pong with the other query tile
         Ring br;          // position of my query tile's next bias tile in the producer's ring
         if (BIAS == 1 && X == 1) br.next(prm.bst);
@@ -356,6 +371,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             const int head = u / prm.ublocks;
             const int ub = u - head * prm.ublocks;
             const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
+            ++usm;
             if (X >= nact) {  // tile B of the last unit of a head with an odd number of 128-row blocks: nothing to do
                 if (BIAS == 1)
                     for (int j = 0; j < T; ++j) br.next(prm.bst);
@@ -369,6 +385,10 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             float m_ref = fast ? sc * kLog2e * (float)d : -INFINITY, m_true = -INFINITY;
             float l0 = 0.f, l1 = 0.f;
             const bool dump = DBG && prm.dbg_S && head == prm.dbg_head;
+            // BIAS 4: my token's grid position and this unit's tables
+            const int rg = BIAS == 4 ? row / prm.g : 0, cg = BIAS == 4 ? row - rg * prm.g : 0;
+            const float* rowtab = &sm->rel2[usm % 3][0][0];
+            const float* coltab = &sm->rel2[usm % 3][1][0];
             float x[32];
             for (int j = 0; j < T; ++j, ++gx) {
                 const uint32_t st = gx & 1u, par = (gx >> 1) & 1u;
@@ -405,6 +425,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     warp_arrive(&sm->bfree[br.stage], lane);
                     br.next(prm.bst);  // tile A and tile B alternate in the ring when both are active
                     if (nact == 2) br.next(prm.bst);
+                }
+                if (BIAS == 4) {
+                    // b = row_offsets[ri - rj + g - 1] + col_offsets[ci - cj + g - 1] (attention.cpp:84-94).  g % 32 == 0, so my 32
+                    // keys lie in one grid row: rj is one value, cj = cj0 + c.  fp32 sum first, then x = dot*sc + b, exactly what
+                    // the dense path computes from the materialised table (bit-identical when the sums are bf16-representable).
+                    const int kb = j * TN + half * 32;
+                    const int rj = kb / prm.g, cj0 = kb - rj * prm.g;
+                    const float rv = rowtab[rg - rj + prm.g - 1];
+                    const float* cw = coltab + (cg - cj0 + prm.g - 1);  // element c reads cw[-c]: consecutive words across the warp
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) x[c] = fmaf(x[c], sc, rv + cw[-c]);
                 }
                 if (RAGGED && j == T - 1) {  // ragged N (its own instantiation: the test and the masking loop cost the others 5-13%): keys at or past N get weight 0 (attention.cpp:285-287 stops the block there)
                     const int nk = nlast - half * 32;  // valid keys among my 32 columns
@@ -594,6 +625,7 @@ template <int KPAD>
 static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
     if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
+    if (bias_mode == 4) return launch_variant2<KPAD, 4, false>(prm, vmap, bmap, stream);
     if (prm.a.N % TN != 0) {
         if (bias_mode == 1) return launch_variant2<KPAD, 1, false, false, true>(prm, vmap, bmap, stream);
         return launch_variant2<KPAD, 0, false, false, true>(prm, vmap, bmap, stream);

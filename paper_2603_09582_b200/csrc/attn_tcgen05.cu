@@ -47,6 +47,7 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
         const int n2 = launch_attn_tc2(a, g_dbg_S, g_dbg_head, g_dbg_T, stream);
         if (n2 != 0) return n2;
     }
+    if (a.bias && a.bias_kind == BA_BIAS_REL2D) return -(int)cudaErrorNotSupported;  // (the C-ABI layer expands the table for this kernel)
     if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 16 != 0)
         return -(int)cudaErrorMisalignedAddress;
     EncodeTiledFn enc = get_encode();

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "binattn_cuda.h"
 
 namespace ba {
@@ -23,7 +25,7 @@ struct FwdArgs {
     const unsigned char* k_exp;  // [BH, ceil(N/64), KPAD/16, 64, 16] e4m3 +-1.0 bytes of K in UMMA tile order (second-generation
                                  // tcgen05 kernel only; nullptr when the workspace has no room for it)
     const void* bias;         // dense: [bias_heads, N, bias_ld]; rel1d: [bias_heads, 2N-1]; or nullptr
-    int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D
+    int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D / BA_BIAS_REL2D ([bias_heads, 2, 2g-1]; tc2 kernel only)
     float* O;                 // [BH, N, d] fp32
     float* row_max;           // [BH, N] or nullptr
     float* row_sum;           // [BH, N] or nullptr

@@ -15,6 +15,7 @@
 #include "ba_common.cuh"
 
 namespace ba {
+int launch_expand_rel2d(const void* tables, int dtype, int heads, int N, int g, float* out, cudaStream_t stream);  // bias_expand.cu
 int launch_pack_signs_qk(const void* Q, const void* K, int in_dtype, int64_t heads, int N, int d, uint64_t* q_words,
                          uint64_t* k_words, float* mu_q, float* mu_k, float* partials, unsigned int* tickets,
                          cudaStream_t stream);
@@ -39,6 +40,11 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int grid_side(int n) {  // g with g*g == n, or 0
+    int g = (int)std::lround(std::sqrt((double)n));
+    return (g > 0 && (long long)g * g == n) ? g : 0;
+}
 
 struct Layout {
     size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, kexp, total;
@@ -80,8 +86,17 @@ int check_params(const ba_params* p, bool need_attention) {
     if (!need_attention) return BA_OK;
     if (!(p->inv_tau > 0.0f) || !(p->inv_tau < INFINITY))  // attention.cpp:24-25
         return fail(BA_ERR_VALIDATION, "attention: temperature must be positive");
-    if (p->bias_mode != BA_BIAS_NONE && p->bias_mode != BA_BIAS_DENSE && p->bias_mode != BA_BIAS_REL1D)
-        return fail(BA_ERR_VALIDATION, "bias_mode must be BA_BIAS_NONE, BA_BIAS_DENSE or BA_BIAS_REL1D");
+    if (p->bias_mode != BA_BIAS_NONE && p->bias_mode != BA_BIAS_DENSE && p->bias_mode != BA_BIAS_REL1D &&
+        p->bias_mode != BA_BIAS_REL2D)
+        return fail(BA_ERR_VALIDATION, "bias_mode must be BA_BIAS_NONE, BA_BIAS_DENSE, BA_BIAS_REL1D or BA_BIAS_REL2D");
+    if (p->bias_mode == BA_BIAS_REL2D) {
+        if (grid_side(p->N) == 0)  // attention.cpp:79-81
+            return fail(BA_ERR_SHAPE, "bias: relative-2d requires N to be a perfect square");
+        if (p->bias_heads != 1 && p->bias_heads != p->H)  // attention.cpp:82-83 (tables must match the head)
+            return fail(BA_ERR_SHAPE, "bias: relative-2d tables must be [1 or H, 2, 2*sqrt(N)-1]");
+        if (p->bias_dtype != BA_BF16 && p->bias_dtype != BA_F32)
+            return fail(BA_ERR_VALIDATION, "bias_dtype must be BA_BF16 or BA_F32");
+    }
     if (p->bias_mode == BA_BIAS_REL1D) {
         if (p->bias_heads != 1 && p->bias_heads != p->H)  // attention.cpp:66-67 (offsets must match the head)
             return fail(BA_ERR_SHAPE, "bias: relative-1d offsets must be [1 or H, 2N-1]");
@@ -120,6 +135,8 @@ struct ba_handle {
     size_t partials_n = 0;
     double* diag = nullptr;     // {mu_q, mu_k} of ba_attention_probs
     size_t diag_bytes = 0;
+    void* rel2d = nullptr;      // Relative2dBias expanded to a dense fp32 [bias_heads, N, N] table (shapes the in-kernel path does not take)
+    size_t rel2d_bytes = 0;
     // host-buffer path: copy-in stream, compute stream, copy-out stream + per-chunk events
     cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
     cudaEvent_t ev_in[kHostChunksMax] = {}, ev_done[kHostChunksMax] = {};
@@ -198,6 +215,7 @@ int ba_destroy(ba_handle* h) {
     if (h->tickets) cudaFree(h->tickets);
     if (h->partials) cudaFree(h->partials);
     if (h->diag) cudaFree(h->diag);
+    if (h->rel2d) cudaFree(h->rel2d);
     for (void* s : h->stage)
         if (s) cudaFree(s);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -329,6 +347,7 @@ int ba_attention_probs(ba_handle* h, const ba_params* p, int mode, const void* Q
     int rc = check_params(p, true);
     if (rc) return rc;
     if (mode != BA_PROBS_FULL && mode != BA_PROBS_BINARY) return fail(BA_ERR_VALIDATION, "attention_probs: unknown mode %d", mode);
+    if (p->bias_mode == BA_BIAS_REL2D) return fail(BA_ERR_UNSUPPORTED, "attention_probs: pass the relative-2d bias as a dense table");
     if (!Q || !K || !rows || !P) return fail(BA_ERR_SHAPE, "attention_probs: NULL pointer");
     if (p->bias_mode != BA_BIAS_NONE && !bias) return fail(BA_ERR_SHAPE, "attention_probs: bias_mode set but bias is NULL");
     if (nrows < 1) return fail(BA_ERR_SHAPE, "attention_probs: nrows must be >= 1");
@@ -433,10 +452,29 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.k_exp = L.total > L.kexp ? reinterpret_cast<const unsigned char*>(ws + L.kexp) : nullptr;
     a.bias = p->bias_mode != BA_BIAS_NONE ? bias : nullptr;
     a.bias_kind = p->bias_mode;
+    a.bias_dtype = p->bias_dtype;
+    a.bias_ld = p->bias_ld ? p->bias_ld : p->N;
+    if (p->bias_mode == BA_BIAS_REL2D) {
+        const int g = grid_side(p->N);
+        const bool in_kernel = kernel == BA_KERNEL_TCGEN05 && !p->quantize_pv && ba::tc2_shape_ok(p->in_dtype, p->N, p->d) &&
+                               g % 32 == 0 && g <= 128 && !(getenv("BA_TC2") && atol(getenv("BA_TC2")) == 0) && a.k_exp &&
+                               reinterpret_cast<uintptr_t>(V) % 16 == 0 && reinterpret_cast<uintptr_t>(O) % 32 == 0;
+        if (!in_kernel) {  // expand once into the handle's fp32 table and run the dense path (attention.cpp:78-96)
+            const size_t need = (size_t)p->bias_heads * p->N * p->N * sizeof(float);
+            int rc = ensure(&h->rel2d, &h->rel2d_bytes, need, false);
+            if (rc) return rc;
+            const int ne = ba::launch_expand_rel2d(bias, p->bias_dtype, p->bias_heads, p->N, g, static_cast<float*>(h->rel2d), stream);
+            if (ne < 0) return fail(BA_ERR_CUDA, "relative-2d expansion launch: %s", cudaGetErrorString((cudaError_t)(-ne)));
+            h->launches += ne;
+            a.bias = h->rel2d;
+            a.bias_kind = BA_BIAS_DENSE;
+            a.bias_dtype = BA_F32;
+            a.bias_ld = p->N;
+        }
+    }
     a.O = O;
     a.row_max = row_max;
     a.row_sum = row_sum;
-    a.bias_ld = p->bias_ld ? p->bias_ld : p->N;
     a.BH = (int)heads;
     a.H = p->H;
     a.N = p->N;
@@ -444,7 +482,6 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.W64 = L.W64;
     a.bias_heads = p->bias_mode != BA_BIAS_NONE ? p->bias_heads : 1;
     a.head0 = (int)(head0 % p->H);
-    a.bias_dtype = p->bias_dtype;
     a.in_dtype = p->in_dtype;
     a.inv_tau = p->inv_tau;
 
@@ -501,6 +538,8 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     if (p->bias_mode == BA_BIAS_DENSE && !bias) return fail(BA_ERR_SHAPE, "bias: dense table must be N x N (got NULL)");
     if (p->bias_mode == BA_BIAS_REL1D && !bias)
         return fail(BA_ERR_SHAPE, "bias: relative-1d offsets must have length 2N-1 (got NULL)");
+    if (p->bias_mode == BA_BIAS_REL2D && !bias)
+        return fail(BA_ERR_SHAPE, "bias: relative-2d tables must have length 2*sqrt(N)-1 (got NULL)");
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     BA_CUDA(cudaSetDevice(h->device));
     int kernel = 0;
@@ -536,6 +575,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     const size_t bias_bytes =
         p->bias_mode == BA_BIAS_DENSE   ? (size_t)p->bias_heads * p->N * ld * ba::dtype_size(p->bias_dtype)
         : p->bias_mode == BA_BIAS_REL1D ? (size_t)p->bias_heads * (2 * (size_t)p->N - 1) * ba::dtype_size(p->bias_dtype)
+        : p->bias_mode == BA_BIAS_REL2D ? (size_t)p->bias_heads * 2 * (2 * (size_t)grid_side(p->N) - 1) * ba::dtype_size(p->bias_dtype)
                                         : 0;
     // chunk plan: sizes ramp up 2 -> 4 -> 8 -> 16 MB (of EACH input) and back down at the end, so the pipeline fills and
     // drains on small chunks while the bulk moves in few large copies (measured on C2: 5.9 ms with uniform 4 MB chunks,
