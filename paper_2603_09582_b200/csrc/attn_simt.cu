@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
                 if (w < w64) diff += __popcll(qb[w] ^ sk[jj * w64 + w]);
             float x2 = (float)(d - 2 * diff) * sc2;
             if (bias_row) x2 = fmaf(load_as_float(bias_row, a.bias_dtype, rel1d ? row - (j0 + jj) + N - 1 : j0 + jj), kLog2e, x2);
+            if (x2 == -INFINITY) continue;  // masked key (bias = -inf): weight 0, and never exp2(-inf - -inf) while m is still -inf
             if (x2 > m) {  // running-max update (attention.cpp:308-324); first key: alpha = exp2(-inf) = 0
                 const float alpha = exp2f(m - x2);
                 l *= alpha;

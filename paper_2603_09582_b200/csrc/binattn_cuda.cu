@@ -149,13 +149,35 @@ struct ba_handle {
 
 namespace {
 
+// Entry points bind to the handle's device for their duration and put the caller's current device back (a process
+// holding handles on several GPUs must not have its current device changed behind its back).
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+#define BA_BIND_DEVICE(h)                                                                                         \
+    DeviceGuard guard_((h)->device);                                                                              \
+    if (guard_.err != cudaSuccess) return fail(BA_ERR_CUDA, "cudaSetDevice(%d): %s", (h)->device, cudaGetErrorString(guard_.err))
+
 int ensure(void** ptr, size_t* have, size_t need, bool zero) {
     if (*have >= need && *ptr) return BA_OK;
     if (*ptr) BA_CUDA(cudaFree(*ptr));
     *ptr = nullptr;
     *have = 0;
     BA_CUDA(cudaMalloc(ptr, need));
-    if (zero) BA_CUDA(cudaMemset(*ptr, 0, need));
+    if (zero) {
+        // The zero fill runs on the legacy default stream; the kernels that count on it run on streams that do not order
+        // against that stream (cudaStreamNonBlocking), so it must have landed before this returns.
+        BA_CUDA(cudaMemset(*ptr, 0, need));
+        BA_CUDA(cudaDeviceSynchronize());
+    }
     *have = need;
     return BA_OK;
 }
@@ -185,7 +207,8 @@ int ba_create(int device, ba_handle** out) {
         return fail(BA_ERR_CUDA, "no CUDA device (%s); this library has no CPU fallback",
                     e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
     if (device < 0 || device >= count) return fail(BA_ERR_VALIDATION, "device %d out of range [0,%d)", device, count);
-    BA_CUDA(cudaSetDevice(device));
+    DeviceGuard guard_(device);
+    if (guard_.err != cudaSuccess) return fail(BA_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(guard_.err));
     cudaDeviceProp prop{};
     BA_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10)
@@ -210,7 +233,11 @@ int ba_create(int device, ba_handle** out) {
 
 int ba_destroy(ba_handle* h) {
     if (!h) return BA_OK;
-    cudaSetDevice(h->device);
+    DeviceGuard guard_(h->device);
+    if (h->prof_ev) {  // ba_profile_begin without ba_profile_end
+        for (int i = 0; i < 3 * h->prof_cap; ++i) cudaEventDestroy(h->prof_ev[i]);
+        delete[] h->prof_ev;
+    }
     if (h->ws) cudaFree(h->ws);
     if (h->tickets) cudaFree(h->tickets);
     if (h->partials) cudaFree(h->partials);
@@ -238,7 +265,7 @@ int64_t ba_launch_count(const ba_handle* h) { return h ? h->launches : 0; }
 
 int ba_profile_begin(ba_handle* h, int max_calls) {
     if (!h || max_calls < 1) return fail(BA_ERR_VALIDATION, "profile_begin: need a handle and max_calls >= 1");
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     if (h->prof_ev) {
         for (int i = 0; i < 3 * h->prof_cap; ++i) cudaEventDestroy(h->prof_ev[i]);
         delete[] h->prof_ev;
@@ -294,7 +321,7 @@ int ba_pack_signs(ba_handle* h, const ba_params* p, const void* X, uint64_t* wor
     int rc = check_params(p, false);
     if (rc) return rc;
     if (!X || !words) return fail(BA_ERR_SHAPE, "pack_signs: X and words must be non-NULL");
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     const Layout L = make_layout(p);
     if ((rc = ensure_tickets(h, 2 * (size_t)L.BH))) return rc;
     size_t have = h->partials_n;
@@ -315,7 +342,7 @@ int ba_quantize_values(ba_handle* h, const ba_params* p, const void* V, int8_t* 
     if (rc) return rc;
     if (!V || !vq || !scales) return fail(BA_ERR_SHAPE, "quantize_values: V, vq and scales must be non-NULL");
     if (p->d > 256) return fail(BA_ERR_UNSUPPORTED, "head dim %d > 256 is not supported", p->d);
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     const int n = ba::launch_quantize_values(V, p->in_dtype, (int64_t)p->B * p->H, p->N, p->d, vq, scales,
                                              static_cast<cudaStream_t>(stream));
     if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
@@ -332,7 +359,7 @@ int ba_binary_logits(ba_handle* h, const ba_params* p, const uint64_t* q_words, 
     const int64_t BH = (int64_t)p->B * p->H;
     if (head_index < 0 || head_index >= BH) return fail(BA_ERR_SHAPE, "binary_logits: head %lld outside [0,%lld)",
                                                         (long long)head_index, (long long)BH);
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     const int W64 = (p->d + 63) / 64;
     const int64_t off = head_index * p->N * W64;
     const int n = ba::launch_binary_logits(q_words + off, k_words + off, p->N, p->d, S, static_cast<cudaStream_t>(stream));
@@ -354,7 +381,7 @@ int ba_attention_probs(ba_handle* h, const ba_params* p, int mode, const void* Q
     const int64_t BH = (int64_t)p->B * p->H;
     if (head_index < 0 || head_index >= BH)
         return fail(BA_ERR_SHAPE, "attention_probs: head %lld outside [0,%lld)", (long long)head_index, (long long)BH);
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     rc = ensure(reinterpret_cast<void**>(&h->diag), &h->diag_bytes, 2 * sizeof(double), false);
     if (rc) return rc;
@@ -391,7 +418,7 @@ int ba_attention_fidelity(ba_handle* h, const double* p_ref, const double* p_oth
     if (keff > ba::fidelity_topk_max())
         return fail(BA_ERR_UNSUPPORTED, "attention_fidelity: min(k, cols) = %lld > %d is not supported", (long long)keff,
                     ba::fidelity_topk_max());
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     double* partial = nullptr;
     BA_CUDA(cudaMalloc(&partial, (size_t)rows * 8 * sizeof(double)));
@@ -424,7 +451,7 @@ int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* 
     if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
     if (!p_ref || !p_other || !out) return fail(BA_ERR_SHAPE, "attention_fidelity: NULL pointer");
     if (rows < 1 || cols < 1) return fail(BA_ERR_SHAPE, "attention_fidelity: shape mismatch");
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     const size_t bytes = (size_t)rows * (size_t)cols * sizeof(double);
     double* dev = nullptr;
     BA_CUDA(cudaMalloc(&dev, 2 * bytes));
@@ -541,7 +568,7 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     if (p->bias_mode == BA_BIAS_REL2D && !bias)
         return fail(BA_ERR_SHAPE, "bias: relative-2d tables must have length 2*sqrt(N)-1 (got NULL)");
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     int kernel = 0;
     if ((rc = resolve_kernel(p, &kernel))) return rc;
     const Layout L = make_layout(p);
@@ -564,7 +591,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     if (rc) return rc;
     if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
     if (p->bias_mode != BA_BIAS_NONE && !bias) return fail(BA_ERR_SHAPE, "bias: table / offsets pointer is NULL");
-    BA_CUDA(cudaSetDevice(h->device));
+    BA_BIND_DEVICE(h);
     int kernel = 0;
     if ((rc = resolve_kernel(p, &kernel))) return rc;
     const size_t BH = (size_t)p->B * p->H;
@@ -646,7 +673,12 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
                        row_max ? reinterpret_cast<float*>(dM + h0 * head_row) : nullptr,
                        row_sum ? reinterpret_cast<float*>(dL + h0 * head_row) : nullptr,
                        static_cast<char*>(h->stage[7]) + (size_t)c * Lc.total, h->tickets + 2 * h0, h->stream, false);
-        if (rc) return rc;
+        if (rc) {  // copies from / to the caller's buffers may still be in flight: drain before handing them back
+            cudaStreamSynchronize(h->stream_in);
+            cudaStreamSynchronize(h->stream);
+            cudaStreamSynchronize(h->stream_out);
+            return rc;
+        }
         BA_CUDA(cudaEventRecord(h->ev_done[c], h->stream));
         BA_CUDA(cudaStreamWaitEvent(h->stream_out, h->ev_done[c], 0));
         BA_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(O) + h0 * head_out, dO + h0 * head_out, nh * head_out,

@@ -68,7 +68,9 @@ __device__ __forceinline__ void bf16x8_signs_abs(const uint4& v, unsigned int& b
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t mag = r[i] & 0x7FFF7FFFu;
-        neg[i] = r[i] & (mag + 0x7FFF7FFFu) & 0x80008000u;
+        // "negative and non-zero", or NaN of either sign (x >= 0.0 is false for NaN, bitops.cpp:45): a half is NaN when its
+        // magnitude exceeds 0x7F80, i.e. when mag + 0x007F carries into bit 15 / 31 (mag <= 0x7FFF: no carry leaves the half)
+        neg[i] = ((r[i] & (mag + 0x7FFF7FFFu)) | (mag + 0x007F007Fu)) & 0x80008000u;
         sa += __uint_as_float(mag << 16);          // |even element|
         sa += __uint_as_float(mag & 0xFFFF0000u);  // |odd element|
     }
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 mag[i] = r[i] & 0x7FFF7FFFu;
-                neg[i] = r[i] & (mag[i] + 0x7FFF7FFFu) & 0x80008000u;  // negative and non-zero (see bf16x8_signs_abs)
+                neg[i] = ((r[i] & (mag[i] + 0x7FFF7FFFu)) | (mag[i] + 0x007F007Fu)) & 0x80008000u;  // negative and non-zero, or NaN (see bf16x8_signs_abs)
             }
             asm volatile(
                 "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%8}, {%0,%1,%2,%3};"

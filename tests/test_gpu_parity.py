@@ -76,6 +76,46 @@ def test_scale_invariance_of_bits(ba, port):  # test_attention.cpp:330-347
     assert (w0 == w1).all() and float(m1) == pytest.approx(7.0 * float(m0), rel=1e-6)
 
 
+def test_pack_signs_nan_maps_to_zero_bit(ba):
+    """bit = 1 iff x >= 0.0 (bitops.cpp:45): NaN of either sign packs as 0 in every kernel variant (the reference itself
+    rejects non-finite inputs, tensor.cpp:15; the ABI has no such check, so the rule must not depend on dtype or d)."""
+    import torch
+    for d in (64, 72, 200):
+        x = torch.randn(1, 2, 70, d, device="cuda")
+        x[0, 0, 3, 5] = float("nan")
+        x[0, 1, 69, d - 1] = -float("nan")
+        x[0, 1, 0, 0] = float("inf")
+        for dt in (torch.bfloat16, torch.float32, torch.float16):
+            xd = x.to(dt)
+            words, _ = ba.pack_signs(xd)
+            w = words_to_numpy(words).reshape(2, 70, -1)
+            want = (xd.float() >= 0).cpu().numpy()
+            got = np.zeros_like(want)
+            for c in range(d):
+                got[0, :, :, c] = ((w[:, :, c // 64] >> np.uint64(c % 64)) & np.uint64(1)).astype(bool)
+            assert np.array_equal(got, want), (d, dt)
+
+
+def test_masked_first_keys_do_not_poison_the_row(ba, port):
+    """Mask-style bias (-inf on the leading keys of some rows): every kernel gives the finite reference answer (the CUDA-core
+    kernel's per-key running max used to evaluate exp2(-inf - -inf) there)."""
+    import torch
+    n, d = 96, 32
+    q, k, v, _ = make_head_inputs(port, 45, 0, n, d)
+    b = np.zeros((n, n))
+    b[5, :40] = -np.inf
+    b[77, :60] = -np.inf   # (under one 64-key block: a fully masked first block is NaN in the reference itself, attention.cpp:308-312)
+    y = port.binary_attention_fused(q, k, v, bias=b)[0]
+    assert np.isfinite(y).all()
+    for dt in ("bf16", "f32"):
+        Q, K, V = (to_torch(x[None, None], dt) for x in (q, k, v))
+        bt = torch.from_numpy(b).to("cuda", torch.float32)[None]
+        for kern in kernels_for(ba, 1, 1, n, d, dt, bt):
+            O = ba.forward(Q, K, V, bt, kernel=kern)
+            assert torch.isfinite(O).all(), kern
+            assert np.abs(O[0, 0].cpu().numpy() - y).max() <= TOL_O, kern
+
+
 def test_pack_is_bit_reproducible(ba, port):
     X = to_torch(make_head_inputs(port, 9, 0, 2000, 128)[0][None, None], "bf16")
     w0, m0 = ba.pack_signs(X)
