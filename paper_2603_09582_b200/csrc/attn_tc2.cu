@@ -17,8 +17,7 @@ EncodeTiledFn get_encode_fn();  // attn_tcgen05.cu
 int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* dbg_T, cudaStream_t stream) {
     using namespace tc2;
     if (env_long("BA_TC2", 1) == 0) return 0;
-    if (!tc2_shape_ok(a.in_dtype, a.N, a.d) || !a.k_exp) return 0;
-    if (a.N < env_long("BA_TC2_MIN_N", 0)) return 0;  // dev knob
+    if (!tc2_shape_ok(a.in_dtype, a.N, a.d) || !a.k_exp || !a.q_exp) return 0;
     if (dbg_S && a.N % TN != 0) return 0;  // (the logits dump has no ragged instantiation)
     if (a.d % 8 != 0 || a.d > 128) return 0;
     if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 32 != 0) return 0;

@@ -19,7 +19,7 @@
 //   (a first version used 128-key tiles with one S stage per query tile and 64 keys per thread; the two query tiles then
 //    ran in phase -- both waiting for the tensor core at the same time -- and the MUFU pipe stayed at 64%)
 // 640 threads: warps 0-15 softmax (104 registers), 16 / 17 MMA issue for tile A / B (16 also allocates TMEM), 18 TMA producer,
-// 19 Q expander.  K tiles come pre-expanded from expand_k_kernel (workspace plane FwdArgs::k_exp) by bulk copy.
+// 19 the Relative2dBias tables.  Q and K tiles come pre-expanded from expand_qk_kernel (workspace planes) by bulk copy.
 // TMEM (512 columns): tile X owns S stages [128 X + 64 s, +64) and O [256 + 128 X, +dvp); the bf16 weights overwrite the
 // S columns their thread has just read: keys 0-31 -> columns [0,16), keys 32-63 -> columns [32,48) of the stage.
 //
@@ -62,7 +62,6 @@ struct Smem2 {
     uint64_t pfull[2][2];         // [query tile][stage] P written by the eight softmax warps of the query tile
     uint64_t pvdone[2][2];        // [query tile][stage] P.V MMA retired
     uint64_t ofree[2];            // O of query tile X read out by the epilogue
-    uint2 lut[256];               // byte of sign bits -> 8 e4m3 +-1.0 bytes
     float xch[2][2][TM];          // (query tile, column half, row): half-row max / partial denominator for the other half
     uint32_t flag[2][2][4][2];    // (tile parity, query tile, lane quadrant, column half): "my warp needs a new reference max"
     float rel2[3][2][256];        // BIAS 4: row / col offset tables (2g-1 <= 255 entries) of the heads of three consecutive units
@@ -117,7 +116,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
     Smem2* sm = reinterpret_cast<Smem2*>(sK + prm.kst * TN * KPAD);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int N = a.N, d = a.d, w64 = a.W64, T = prm.tiles;
+    const int N = a.N, d = a.d, T = prm.tiles;
     const int G = gridDim.x;
     // dev timeline (TL builds): [cta][role 0 = softmax warp 0 (tile A), 1 = MMA warp, 2 = TMA lane, 3 = expander][kTlStamps]
     long long* tl_buf = nullptr;
@@ -128,7 +127,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
 
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm->qfull[s], 1);
+            mbar_init(&sm->qfull[s], BIAS == 4 ? 2 : 1);  // the producer's expect_tx arrival (+ warp 19 with the BIAS 4 tables)
             mbar_init(&sm->qfree[s], 2);
             mbar_init(&sm->ofree[s], 8);
             for (int t = 0; t < 2; ++t) {
@@ -158,7 +157,6 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
         if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
     }
-    if (tid < 256) sm->lut[tid] = expand_byte((uint32_t)tid);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -285,12 +283,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         } else if (warp == 18) {
             // ======================================================== TMA producer: bias tiles, V tiles
             if (lane == 0) {
-                Ring vr, br, kr;
+                Ring vr, br, kr, qr;
                 for (int u = blockIdx.x; u < prm.units; u += G) {
                     const int head = u / prm.ublocks;
                     const int ub = u - head * prm.ublocks;
                     const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
                     const int bh = (a.head0 + head) % a.H % a.bias_heads;
+                    // the unit's two Q tiles, already expanded (expand_qk_kernel): one bulk copy
+                    mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
+                    mbar_expect_tx(&sm->qfull[qr.stage], 2 * TM * KPAD);
+                    bulk_load(sQ + qr.stage * 2 * TM * KPAD, a.q_exp + (int64_t)u * (2 * TM * KPAD), 2 * TM * KPAD, &sm->qfull[qr.stage]);
+                    qr.next(prm.qst);
                     for (int j = 0; j < T; ++j) {
                         if (BIAS == 1) {
                             for (int X = 0; X < nact; ++X) {
@@ -314,39 +317,25 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 }
             }
         } else {
-            // ======================================================== Q expander (one warp; the K tiles arrive expanded, by bulk copy:
-            // expanding 64 keys per tile in here took one warp ~1500 clk per tile and two warps ~1400 -- against 1024 clk of
-            // exponentials -- and was what every earlier build of this kernel was really waiting for)
-            Ring qr;
-            int ui = 0;  // units of this CTA so far
-            for (int u = blockIdx.x; u < prm.units; u += G, ++ui) {
-                const int head = u / prm.ublocks;
-                const int row0 = (u - head * prm.ublocks) * 2 * TM;
-                mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
-                if (BIAS == 4) {
-                    // Relative2dBias tables of the unit's head (attention.hpp:22-26), published with the Q stage: the softmax
-                    // warps read them after the first S of the unit (qfull -> MMA -> sfull orders the accesses).  Three slots:
-                    // slot ui % 3 is rewritten for unit ui + 3, i.e. after every S MMA of unit ui + 1 has retired (qfree), by
-                    // which time the softmax warps have long left unit ui (its last P precedes the next unit's third S).
+            // ======================================================== warp 19: Relative2dBias tables (BIAS 4); idle otherwise
+            if (BIAS == 4) {
+                Ring qr;
+                int ui = 0;  // units of this CTA so far
+                for (int u = blockIdx.x; u < prm.units; u += G, ++ui) {
+                    const int head = u / prm.ublocks;
+                    mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
+                    // tables of the unit's head (attention.hpp:22-26), published with the Q stage (qfull counts this warp too): the
+                    // softmax warps read them after the first S of the unit (qfull -> MMA -> sfull orders the accesses).  Three
+                    // slots: slot ui % 3 is rewritten for unit ui + 3, i.e. after every S MMA of unit ui + 1 has retired (qfree),
+                    // by which time the softmax warps have long left unit ui (its last P precedes the next unit's third S).
                     const int len = 2 * prm.g - 1;
                     const int bh = (a.head0 + head) % a.H % a.bias_heads;
                     const char* tb = static_cast<const char*>(a.bias) + (size_t)bh * 2 * len * dtype_size(a.bias_dtype);
                     float* dst = &sm->rel2[ui % 3][0][0];
                     for (int i = lane; i < 2 * len; i += 32) dst[(i >= len ? 256 - len : 0) + i] = load_as_float(tb, a.bias_dtype, i);
+                    warp_arrive(&sm->qfull[qr.stage], lane);
+                    qr.next(prm.qst);
                 }
-                unsigned char* qt = sQ + qr.stage * 2 * TM * KPAD;
-#pragma unroll 1
-                for (int i = 0; i < 8; i += 2) {  // the unit's 256 query rows, two per lane and pass (rows past N expand to zeros)
-                    uint32_t wq0[KPAD / 32], wq1[KPAD / 32];
-                    const int r0 = lane + 32 * i, r1 = r0 + 32;
-                    load_words<KPAD>(wq0, a.q_words + ((int64_t)head * N + row0 + r0) * w64, w64, row0 + r0 < N);
-                    load_words<KPAD>(wq1, a.q_words + ((int64_t)head * N + row0 + r1) * w64, w64, row0 + r1 < N);
-                    expand_store<KPAD>(qt + (r0 >> 7) * TM * KPAD, TM, r0 & 127, wq0, d, row0 + r0 < N, sm->lut);
-                    expand_store<KPAD>(qt + (r1 >> 7) * TM * KPAD, TM, r1 & 127, wq1, d, row0 + r1 < N, sm->lut);
-                }
-                fence_proxy_async();
-                warp_arrive(&sm->qfull[qr.stage], lane);
-                qr.next(prm.qst);
             }
         }
     } else {
@@ -545,34 +534,42 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
     }
 }
 
-// K sign planes -> e4m3 +-1.0 bytes in the order the S MMA reads them (K-major, no swizzle, 8 x 16 B core matrices):
-// byte (key r, element kb) of 64-key tile t of a head lives at t*64*KPAD + (kb/16)*(64*16) + r*16 + kb%16; elements at or past d
-// are 0.0.  One thread per 16-byte chunk; a warp writes 512 consecutive bytes.
+// Sign planes -> e4m3 +-1.0 bytes in the order the S MMA reads them (K-major, no swizzle, 8 x 16 B core matrices), one launch
+// for both operands (blockIdx.y = 0: K in 64-key tiles, 1: Q in 128-row tiles, two per 256-row unit):
+// byte (row r, element kb) of tile t of a head lives at t*R*KPAD + (kb/16)*(R*16) + r*16 + kb%16 (R = 64 or 128); rows at or
+// past N (ragged last tile / unit) and elements at or past d are 0.0.  One thread per 16-byte chunk; a warp writes 512
+// consecutive bytes.  (Expanding in the attention kernel -- one or two warps, through a lookup table -- took longer per key
+// tile than the tile's exponentials and ~5000 clk per unit for Q: it was what the kernel was really waiting for.)
 template <int KPAD>
-__global__ void __launch_bounds__(256) expand_k_kernel(const uint64_t* __restrict__ words, unsigned char* __restrict__ out, int64_t heads,
-                                                       int N, int tiles, int w64, int d) {
+__global__ void __launch_bounds__(256) expand_qk_kernel(const uint64_t* __restrict__ q_words, const uint64_t* __restrict__ k_words,
+                                                        unsigned char* __restrict__ q_out, unsigned char* __restrict__ k_out,
+                                                        int64_t heads, int N, int ktiles, int qtiles, int w64, int d) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int C = KPAD / 16;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = ((head * tiles + tile) * C + c) * 64 + r
-    if (idx >= heads * tiles * C * 64) return;
-    const int r = (int)(idx & 63);
-    const int c = (int)((idx >> 6) % C);
-    const int64_t ht = (idx >> 6) / C;  // head * tiles + tile
+    const bool isq = blockIdx.y == 1;
+    const int R = isq ? 128 : 64, sh = isq ? 7 : 6, tiles = isq ? qtiles : ktiles;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = ((head * tiles + tile) * C + c) * R + r
+    if (idx >= heads * tiles * C * R) return;
+    const int r = (int)(idx & (R - 1));
+    const int c = (int)((idx >> sh) % C);
+    const int64_t ht = (idx >> sh) / C;  // head * tiles + tile
     const int64_t head = ht / tiles;
-    const int key = (int)(ht - head * tiles) * 64 + r;  // keys at or past N (last tile of a ragged head) expand to zeros
-    const bool valid = key < N;
-    const uint64_t w = (valid && (c >> 2) < w64) ? __ldg(words + (head * N + key) * w64 + (c >> 2)) : 0ull;
+    const int row = (int)(ht - head * tiles) * R + r;
+    const bool valid = row < N;
+    const uint64_t* words = isq ? q_words : k_words;
+    const uint64_t w = (valid && (c >> 2) < w64) ? __ldg(words + (head * N + row) * w64 + (c >> 2)) : 0ull;
     const uint32_t bits16 = (uint32_t)(w >> (16 * (c & 3))) & 0xFFFFu;
     const uint2 lo = (valid && 16 * c < d) ? expand_byte(bits16 & 0xFF) : make_uint2(0, 0);
     const uint2 hi = (valid && 16 * c + 8 < d) ? expand_byte(bits16 >> 8) : make_uint2(0, 0);
-    reinterpret_cast<uint4*>(out)[idx] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+    reinterpret_cast<uint4*>(isq ? q_out : k_out)[idx] = make_uint4(lo.x, lo.y, hi.x, hi.y);
 }
 
 template <int KPAD>
-static int launch_expand_k(const FwdArgs& a, int tiles, cudaStream_t stream) {
-    const int64_t chunks = (int64_t)a.BH * tiles * (KPAD / 16) * 64;
-    expand_k_kernel<KPAD><<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(a.k_words, const_cast<unsigned char*>(a.k_exp), a.BH, a.N, tiles,
-                                                                              a.W64, a.d);
+static int launch_expand_qk(const FwdArgs& a, int ktiles, int ublocks, cudaStream_t stream) {
+    const int64_t qchunks = (int64_t)a.BH * ublocks * 2 * (KPAD / 16) * 128;  // >= the K plane's chunk count
+    dim3 grid((unsigned)((qchunks + 255) / 256), 2);
+    expand_qk_kernel<KPAD><<<grid, 256, 0, stream>>>(a.q_words, a.k_words, const_cast<unsigned char*>(a.q_exp),
+                                                     const_cast<unsigned char*>(a.k_exp), a.BH, a.N, ktiles, 2 * ublocks, a.W64, a.d);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }
@@ -615,7 +612,7 @@ static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vm
 
 template <int KPAD>
 static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
-    const int ne = launch_expand_k<KPAD>(prm.a, prm.tiles, stream);
+    const int ne = launch_expand_qk<KPAD>(prm.a, prm.tiles, prm.ublocks, stream);
     if (ne < 0) return ne;
     const int nk = launch_main2<KPAD>(prm, bias_mode, vmap, bmap, stream);
     return nk < 0 ? nk : ne + nk;
@@ -623,7 +620,10 @@ static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vm
 
 template <int KPAD>
 static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
-    if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
+    if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) {
+        if (prm.a.N % TN != 0 && KPAD == 64) return launch_variant2<KPAD, 0, false, true, true>(prm, vmap, bmap, stream);
+        return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
+    }
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
     if (bias_mode == 4) return launch_variant2<KPAD, 4, false>(prm, vmap, bmap, stream);
     if (prm.a.N % TN != 0) {

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "binattn_cuda.h"
 
@@ -24,6 +25,7 @@ struct FwdArgs {
     const float* mu_k;        // [BH]
     const unsigned char* k_exp;  // [BH, ceil(N/64), KPAD/16, 64, 16] e4m3 +-1.0 bytes of K in UMMA tile order (second-generation
                                  // tcgen05 kernel only; nullptr when the workspace has no room for it)
+    const unsigned char* q_exp;  // [BH, ceil(N/256), 2, KPAD/16, 128, 16] the same for Q in 128-row tiles, two per unit
     const void* bias;         // dense: [bias_heads, N, bias_ld]; rel1d: [bias_heads, 2N-1]; or nullptr
     int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D / BA_BIAS_REL2D ([bias_heads, 2, 2g-1]; tc2 kernel only)
     float* O;                 // [BH, N, d] fp32
@@ -51,10 +53,15 @@ int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, i
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
 // Shapes the second-generation tcgen05 kernel (attn_tc2.cuh) takes; decides whether the workspace carries the expanded K plane.
 inline bool tc2_shape_ok(int in_dtype, int N, int d) {
-    return in_dtype == BA_BF16 && d % 8 == 0 && d <= 128 && N >= 512;  // below ~512 keys the first-generation kernel is faster (measured)
+    const char* e = getenv("BA_TC2_MIN_N");  // dev knob; default: below ~512 keys the first-generation kernel is faster (measured)
+    const int min_n = e ? atoi(e) : 512;
+    return in_dtype == BA_BF16 && d % 8 == 0 && d <= 128 && N >= (min_n < 128 ? 128 : min_n);
 }
 inline size_t tc2_kexp_bytes(int64_t heads, int N, int d) {  // whole 64-key tiles per head
     return (size_t)heads * ((N + 63) / 64 * 64) * ((d + 31) / 32 * 32);
+}
+inline size_t tc2_qexp_bytes(int64_t heads, int N, int d) {  // whole 256-row units per head
+    return (size_t)heads * ((N + 255) / 256 * 256) * ((d + 31) / 32 * 32);
 }
 // diagnostics (fidelity.cu)
 int launch_head_mean_abs(const void* Q, const void* K, int dtype, int64_t count, double* mu, cudaStream_t stream);

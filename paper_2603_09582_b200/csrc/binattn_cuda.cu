@@ -47,7 +47,7 @@ int grid_side(int n) {  // g with g*g == n, or 0
 }
 
 struct Layout {
-    size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, kexp, total;
+    size_t q_words, k_words, mu_q, mu_k, partials, vq, vscales, kexp, qexp, total;
     int64_t BH;
     int W64, chunks;
 };
@@ -70,8 +70,12 @@ Layout make_layout(const ba_params* p, int64_t heads = -1) {
         L.vscales = off; off += align_up((size_t)L.BH * p->d * sizeof(double), 256);
     }
     L.kexp = off;  // expanded K plane of the second-generation tcgen05 kernel (e4m3 +-1.0 bytes, UMMA tile order)
-    if (!p->quantize_pv && p->kernel != BA_KERNEL_SIMT && ba::tc2_shape_ok(p->in_dtype, p->N, p->d))
+    L.qexp = off;
+    if (!p->quantize_pv && p->kernel != BA_KERNEL_SIMT && ba::tc2_shape_ok(p->in_dtype, p->N, p->d)) {
         off += align_up(ba::tc2_kexp_bytes(L.BH, p->N, p->d), 256);
+        L.qexp = off;
+        off += align_up(ba::tc2_qexp_bytes(L.BH, p->N, p->d), 256);
+    }
     L.total = off;
     return L;
 }
@@ -477,6 +481,7 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.mu_q = reinterpret_cast<float*>(ws + L.mu_q);
     a.mu_k = reinterpret_cast<float*>(ws + L.mu_k);
     a.k_exp = L.total > L.kexp ? reinterpret_cast<const unsigned char*>(ws + L.kexp) : nullptr;
+    a.q_exp = L.total > L.kexp ? reinterpret_cast<const unsigned char*>(ws + L.qexp) : nullptr;
     a.bias = p->bias_mode != BA_BIAS_NONE ? bias : nullptr;
     a.bias_kind = p->bias_mode;
     a.bias_dtype = p->bias_dtype;

@@ -12,6 +12,7 @@ Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in ra
 bias = (0.5 * torch.randn(H, N, (N + 7) // 8 * 8, device="cuda")).to(torch.bfloat16)[:, :, :N] if use_bias else None
 units = B * H * ((N + 127) // 128)
 ctas = min(units, 2 * torch.cuda.get_device_properties(0).multi_processor_count)
+NST = int(sys.argv[6]) if len(sys.argv) > 6 else 64
 for _ in range(3):
     ba.forward(Q, K, V, bias, kernel="tcgen05")
 Tl = torch.zeros(ctas, 4, ST, dtype=torch.int64, device="cuda")
@@ -26,5 +27,5 @@ for cta in [0, ctas // 2]:
     print(f"=== CTA {cta}  (cycles since CTA start; {units} units over {ctas} CTAs)")
     for r in range(4):
         st = tl[cta, r]; st = st[st > 0] - t0
-        print(f"  {names[r]:9s} abs  ", " ".join(str(int(x)) for x in st[:64]))
-        print(f"  {names[r]:9s} diff ", " ".join(str(int(x)) for x in np.diff(st[:64])))
+        print(f"  {names[r]:9s} abs  ", " ".join(str(int(x)) for x in st[:NST]))
+        print(f"  {names[r]:9s} diff ", " ".join(str(int(x)) for x in np.diff(st[:NST])))
