@@ -88,7 +88,14 @@ typedef struct {
     int32_t block_cols;  /* key-block size of the quantize_pv=1 path (AttentionConfig::block_cols, attention.cpp:50-51):
                             the u8 weight grid is relative to the running max after each block, so the result depends
                             on it exactly as the reference's does.  0 -> min(64, N); at most 64.  Ignored otherwise. */
+    int64_t unit_begin;  /* Launcher partition finer than heads: when unit_end > unit_begin,              */
+    int64_t unit_end;    /* ba_binary_attention_fwd computes ONLY the query rows of units [unit_begin, unit_end) of the flattened
+                            (b, h, BA_UNIT_ROWS-row block) grid -- B*H*ceil(N/BA_UNIT_ROWS) units, see ba_shard_units -- and leaves
+                            every other row of O / row_max / row_sum untouched.  A range may split a head: K, V and the
+                            per-head scales of every head it touches are still processed whole.  0, 0 = all units. */
 } ba_params;
+
+#define BA_UNIT_ROWS 256 /* query rows of one shard unit (one unit of the second-generation kernel, two of the first's) */
 
 typedef struct ba_handle ba_handle;
 
@@ -153,6 +160,11 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
 /* Launcher partition: contiguous range of the flattened B*H head grid owned by
  * `rank` of `world` single-GPU processes.  No collective is needed on the hot path. */
 int ba_shard_range(int64_t total_heads, int world, int rank, int64_t* begin, int64_t* end);
+
+/* The same partition over (head, row-block) units for grids with few heads per GPU (BASELINE.json configs[4]: 16 heads over
+ * 8 GPUs): contiguous range of the B*H*ceil(N/BA_UNIT_ROWS) units owned by `rank`; pass it as ba_params.unit_begin/unit_end.
+ * Ranks that share a head each process that head's K and V; inputs are resident per GPU, so nothing is exchanged. */
+int ba_shard_units(const ba_params* p, int world, int rank, int64_t* unit_begin, int64_t* unit_end);
 
 /* Which kernel ba_binary_attention_fwd would run for these params (resolves BA_KERNEL_AUTO). */
 int ba_select_kernel(const ba_params* p);

@@ -9,8 +9,8 @@ a GPU (so the build can be checked), every compute call needs one.
 from .api import (BinaryAttention, BinAttnError, ShapeError, ValidationError, CudaError, UnsupportedError,
                   binary_attention, binary_attention_fused, AttentionConfig, AttentionOutput, Relative1dBias, Relative2dBias,
                   FidelityReport, load_library)
-from .launcher import shard_range, shard_heads, shard_plan, ShardedBinaryAttention
+from .launcher import shard_range, shard_heads, shard_plan, shard_units, ShardedBinaryAttention
 
 __all__ = ["BinaryAttention", "BinAttnError", "ShapeError", "ValidationError", "CudaError", "UnsupportedError",
            "binary_attention", "binary_attention_fused", "AttentionConfig", "AttentionOutput", "Relative1dBias", "Relative2dBias", "FidelityReport", "load_library",
-           "shard_range", "shard_heads", "shard_plan", "ShardedBinaryAttention"]
+           "shard_range", "shard_heads", "shard_plan", "shard_units", "ShardedBinaryAttention"]

@@ -52,7 +52,7 @@ class _Params(C.Structure):
     _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("N", C.c_int32), ("d", C.c_int32), ("in_dtype", C.c_int32),
                 ("bias_mode", C.c_int32), ("bias_heads", C.c_int32), ("bias_dtype", C.c_int32),
                 ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32),
-                ("quantize_pv", C.c_int32), ("block_cols", C.c_int32)]
+                ("quantize_pv", C.c_int32), ("block_cols", C.c_int32), ("unit_begin", C.c_int64), ("unit_end", C.c_int64)]
 
 
 _lib = None
@@ -94,6 +94,7 @@ def load_library() -> C.CDLL:
     lib.ba_attention_fidelity.argtypes = [vp, vp, vp, i64, i64, i64, C.POINTER(_Fidelity), vp]
     lib.ba_binary_attention_host.argtypes = [vp, C.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp]
     lib.ba_shard_range.argtypes = [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
+    lib.ba_shard_units.argtypes = [C.POINTER(_Params), C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
     lib.ba_select_kernel.argtypes = [C.POINTER(_Params)]
     lib.ba_launch_count.argtypes = [vp]
     lib.ba_launch_count.restype = i64
@@ -274,6 +275,13 @@ class BinaryAttention:
         _check(self.lib.ba_profile_end(self.h, C.byref(n), C.byref(a), C.byref(b)))
         return n.value, a.value, b.value
 
+    def shard_units(self, B, H, N, world, rank):
+        """ba_shard_units: this rank's contiguous range of the B*H*ceil(N/256) (head, 256-row block) units."""
+        p = _Params(B=B, H=H, N=N, d=1)
+        b, e = C.c_int64(), C.c_int64()
+        _check(self.lib.ba_shard_units(C.byref(p), world, rank, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
     def select_kernel(self, B, H, N, d, dtype=torch.bfloat16, bias=None) -> str:
         p = self._params(B, H, N, d, dtype, bias)
         k = self.lib.ba_select_kernel(C.byref(p))
@@ -344,10 +352,13 @@ class BinaryAttention:
         _check(self.lib.ba_attention_fidelity(self.h, _ptr(a), _ptr(b), a.shape[0], a.shape[1], int(k), C.byref(out), self._stream()))
         return FidelityReport(out.cos_sim, out.relative_l1, out.rmse, out.precision_at_k, int(k))
 
-    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False, quantize_pv=False, block_cols=None):
+    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False, quantize_pv=False, block_cols=None,
+                units=None, out=None):
         """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output).
         quantize_pv=True selects the reference's default u8 x s8 integer P.V mode (attention.hpp:35; CUDA-core kernel);
-        block_cols is that mode's key-block size (default min(64, N), like AttentionConfig::make)."""
+        block_cols is that mode's key-block size (default min(64, N), like AttentionConfig::make).
+        units=(begin, end): compute only those (head, 256-row block) units of the flattened grid (ba_shard_units); the other
+        rows of `out` (zeros when not given) are left untouched."""
         if Q.dim() != 4:
             raise ShapeError("attention: Q must be [B,H,N,d]")
         if K.shape != Q.shape:
@@ -360,7 +371,18 @@ class BinaryAttention:
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
         bias, bias_t = self._check_bias(bias, H, N)
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel, quantize_pv, block_cols)
-        O = torch.empty((B, H, N, d), dtype=torch.float32, device=Q.device)
+        if units is not None:
+            p.unit_begin, p.unit_end = int(units[0]), int(units[1])
+            if p.unit_begin == p.unit_end:
+                p.unit_begin = p.unit_end = -1  # (0, 0 means "everything" in the ABI; an empty range must stay empty)
+        if out is not None:
+            if out.shape != (B, H, N, d) or out.dtype != torch.float32 or not out.is_contiguous():
+                raise ShapeError("attention: out must be a contiguous float32 [B,H,N,d] tensor")
+            O = out
+        else:
+            O = (torch.zeros if units is not None else torch.empty)((B, H, N, d), dtype=torch.float32, device=Q.device)
+        if units is not None and p.unit_begin < 0:
+            return O
         m = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
         l = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
         _check(self.lib.ba_binary_attention_fwd(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias_t), _ptr(O),

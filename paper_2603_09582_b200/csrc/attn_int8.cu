@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kI8MaxBc * dp);       // [kI8MaxBc][W64]
     int8_t* sv = reinterpret_cast<int8_t*>(smem_raw);
     const int head = blockIdx.x / row_blocks, rb = blockIdx.x - head * row_blocks;
+    if (!row_in_units(a, head, rb * kI8Rows)) return;  // unit-sharded call (kI8Rows divides 256)
     const int tx = threadIdx.x, sl = threadIdx.y;
     const int tid = sl * kI8Rows + tx, nthreads = kI8Rows * ns;
     const int row = rb * kI8Rows + tx;

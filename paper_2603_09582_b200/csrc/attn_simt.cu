@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
 
     const int head = blockIdx.x / row_blocks;
     const int rb = blockIdx.x - head * row_blocks;
+    if (!row_in_units(a, head, rb * kSimtRows)) return;  // unit-sharded call (kSimtRows divides 256: a block lies in one unit)
     const int tx = threadIdx.x, sl = threadIdx.y;
     const int tid = sl * kSimtRows + tx, nthreads = kSimtRows * ns;
     const int row = rb * kSimtRows + tx;

@@ -40,6 +40,12 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     prm.tiles = (a.N + TN - 1) / TN;
     prm.ublocks = (a.N + 2 * TM - 1) / (2 * TM);
     prm.units = a.BH * prm.ublocks;
+    prm.unit0 = 0;
+    if (a.unit1 > 0) {  // unit-sharded call: the shard unit IS this kernel's unit
+        prm.unit0 = a.unit0;
+        prm.units = std::min(a.unit1, a.BH * prm.ublocks);
+        if (prm.units <= prm.unit0) return 0;
+    }
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
     prm.dbg_S = dbg_S;

@@ -72,7 +72,8 @@ struct Params2 {
     FwdArgs a;
     int tiles;     // N / 64 key tiles
     int ublocks;   // ceil(N / 256) units per head
-    int units;     // BH * ublocks
+    int units;     // END (exclusive) of this call's unit range: BH * ublocks unless unit-sharded (ba_params.unit_begin / unit_end)
+    int unit0;     // first unit of the range
     int dvp;       // d rounded up to 16
     int nbox;      // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;
@@ -118,6 +119,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = a.N, d = a.d, T = prm.tiles;
     const int G = gridDim.x;
+    const int ub0 = prm.unit0 + (int)blockIdx.x;  // this CTA's first unit
     // dev timeline (TL builds): [cta][role 0 = softmax warp 0 (tile A), 1 = MMA warp, 2 = TMA lane, 3 = expander][kTlStamps]
     long long* tl_buf = nullptr;
     int tl_n = 0;
@@ -190,7 +192,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             uint32_t up = 0;  // units of my query tile whose last P.V has been issued
             int pend = 0, pj = 0, pact = 0, pvs = 0;
             uint32_t pvph = 0;
-            for (int u = blockIdx.x; u < prm.units; u += G) {
+            for (int u = ub0; u < prm.units; u += G) {
                 const int ub = u % prm.ublocks;
                 const int act = (X == 0 || ub * 2 * TM + TM < N) ? 1 : 0;  // tile B of a head's last unit may be empty: keep the rings moving
                 mbar_wait(&sm->qfull[qr.stage], qr.phase);
@@ -284,7 +286,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             // ======================================================== TMA producer: bias tiles, V tiles
             if (lane == 0) {
                 Ring vr, br, kr, qr;
-                for (int u = blockIdx.x; u < prm.units; u += G) {
+                for (int u = ub0; u < prm.units; u += G) {
                     const int head = u / prm.ublocks;
                     const int ub = u - head * prm.ublocks;
                     const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
@@ -321,7 +323,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             if (BIAS == 4) {
                 Ring qr;
                 int ui = 0;  // units of this CTA so far
-                for (int u = blockIdx.x; u < prm.units; u += G, ++ui) {
+                for (int u = ub0; u < prm.units; u += G, ++ui) {
                     const int head = u / prm.ublocks;
                     mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
                     // tables of the unit's head (attention.hpp:22-26), published with the Q stage (qfull counts this warp too): the
@@ -356,7 +358,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         uint32_t np = 0;  // tiles done in ping-pong with the other query tile
         Ring br;          // position of my query tile's next bias tile in the producer's ring
         if (BIAS == 1 && X == 1) br.next(prm.bst);
-        for (int u = blockIdx.x; u < prm.units; u += G) {
+        for (int u = ub0; u < prm.units; u += G) {
             const int head = u / prm.ublocks;
             const int ub = u - head * prm.ublocks;
             const int nact = (ub * 2 * TM + TM < N) ? 2 : 1;
@@ -591,8 +593,8 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
         if (e != cudaSuccess) return -(int)e;
         configured[dev] = true;
     }
-    int grid = (int)std::min<long>(prm.units, sm_count());
-    if (env_long("BA_GRID", 0) > 0) grid = (int)std::min<long>(prm.units, env_long("BA_GRID", 0));  // dev knob
+    int grid = (int)std::min<long>(prm.units - prm.unit0, sm_count());
+    if (env_long("BA_GRID", 0) > 0) grid = (int)std::min<long>(prm.units - prm.unit0, env_long("BA_GRID", 0));  // dev knob
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads2);

@@ -66,6 +66,14 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
     }
     prm.vbox = prm.fold ? 8192 + 2048 : 8192;
     prm.units = a.BH * prm.mblocks;
+    prm.unit0 = 0;
+    if (a.unit1 > 0) {  // unit-sharded call: the 128-row units covered by the 256-row shard units [unit0, unit1) of this call's heads
+        const int upb = units_per_head(a.N);
+        auto first128 = [&](int g) { return g >= a.BH * upb ? a.BH * prm.mblocks : (g / upb) * prm.mblocks + std::min(2 * (g % upb), prm.mblocks); };
+        prm.unit0 = first128(a.unit0);
+        prm.units = first128(a.unit1);
+        if (prm.units <= prm.unit0) return 1 - 1;  // nothing to do
+    }
     prm.dvp = (a.d + 15) / 16 * 16;
     prm.nbox = (a.d + 63) / 64;
     prm.o_vec8 = reinterpret_cast<uintptr_t>(a.O) % 32 == 0 ? 1 : 0;  // d % 8 == 0 keeps every row 32-byte aligned

@@ -278,7 +278,8 @@ struct Params {
     FwdArgs a;
     int mblocks;       // ceil(N / BM)
     int tiles;         // ceil(N / BN)
-    int units;         // BH * mblocks
+    int units;         // END (exclusive) of this call's range of (head, 128-query block) units: BH * mblocks unless unit-sharded
+    int unit0;         // first unit of the range (0 unless unit-sharded, ba_params.unit_begin)
     int dvp;           // d rounded up to 16 (UMMA N of P.V)
     int nbox;          // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;  // ring depths in shared memory
@@ -647,6 +648,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = a.N, d = a.d, w64 = a.W64, T = prm.tiles;
     const int G = gridDim.x;
+    const int ub0 = prm.unit0 + (int)blockIdx.x;  // this CTA's first unit
     const int ocols = prm.dvp + (ROWSUM ? 16 : 0);  // TMEM columns of the O accumulator (+ denominator block)
     long long* tl_buf = (TL && prm.dbg_T) ? prm.dbg_T + (size_t)blockIdx.x * 4 * kTlStamps : nullptr;
     int tl_n = 0;
@@ -750,7 +752,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
             BA_STAMP(1);
         };
         int unit_i = 0;
-        for (int u = blockIdx.x; u < prm.units; u += G, ++unit_i) {
+        for (int u = ub0; u < prm.units; u += G, ++unit_i) {
             mbar_wait(&sm->qfull[qr.stage], qr.phase);
             const uint64_t qd = q_desc + (uint64_t)((qr.stage * BM * KPAD) >> 4);
             for (int j = 0; j < T; ++j) {
@@ -785,7 +787,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         // ============================================================ TMA producer (V tiles, bias tiles / windows)
         if (lane == 0) {
             Ring vr, br;
-            for (int u = blockIdx.x; u < prm.units; u += G) {
+            for (int u = ub0; u < prm.units; u += G) {
                 const int head = u / prm.mblocks;
                 const int row0 = (u - head * prm.mblocks) * BM;
                 const int bh = (a.head0 + head) % a.H % a.bias_heads;
@@ -818,16 +820,16 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         Ring qr, kr, wr, fr;
         uint32_t wq0[KPAD / 32], wq1[KPAD / 32], wk[KPAD / 32];
         uint32_t wf[FOLD ? KPAD / 32 : 1];  // folded tail: thread t < fold holds the packed words of key T*64 + t
-        if ((int)blockIdx.x < prm.units) {  // words of the first unit
-            const int head = blockIdx.x / prm.mblocks;
-            const int row0 = (blockIdx.x - head * prm.mblocks) * BM;
+        if (ub0 < prm.units) {  // words of the first unit
+            const int head = ub0 / prm.mblocks;
+            const int row0 = (ub0 - head * prm.mblocks) * BM;
             if constexpr (FOLD)
                 if (warp == 6) load_words<KPAD>(wf, a.k_words + ((int64_t)head * N + T * BN + t) * w64, w64, t < prm.fold);
             load_words<KPAD>(wq0, a.q_words + ((int64_t)head * N + row0 + t) * w64, w64, row0 + t < N);
             load_words<KPAD>(wq1, a.q_words + ((int64_t)head * N + row0 + t + 64) * w64, w64, row0 + t + 64 < N);
             load_words<KPAD>(wk, a.k_words + ((int64_t)head * N + t) * w64, w64, t < N);
         }
-        for (int u = blockIdx.x; u < prm.units; u += G) {
+        for (int u = ub0; u < prm.units; u += G) {
             const int head = u / prm.mblocks;
             const int row0 = (u - head * prm.mblocks) * BM;
             mbar_wait(&sm->qfree[qr.stage], qr.phase ^ 1u);
@@ -913,8 +915,8 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         // per-head scales are fetched one unit ahead and only combined when used (an early multiply would stall this
         // in-order thread on the global loads)
         float muq_next = 0.f, muk_next = 0.f;
-        if ((int)blockIdx.x < prm.units) {
-            const int head = blockIdx.x / prm.mblocks;
+        if (ub0 < prm.units) {
+            const int head = ub0 / prm.mblocks;
             muq_next = __ldg(a.mu_q + head);
             muk_next = __ldg(a.mu_k + head);
         }
@@ -926,7 +928,7 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         // x holds the raw scores of the tile about to be processed; its TMEM loads are issued one tile ahead (by the
         // rolling refill inside the previous tile's exponentials when S was ready in time, else right after that tile)
         float x[BN];
-        const int my_units = (prm.units - (int)blockIdx.x + G - 1) / G;
+        const int my_units = (prm.units - ub0 + G - 1) / G;
         const uint32_t total_tiles = (uint32_t)(my_units > 0 ? my_units : 0) * (uint32_t)T;
         if (total_tiles > 0) {
             mbar_wait(&sm->sfull[0], 0);
@@ -939,10 +941,10 @@ attn_tc_kernel(const __grid_constant__ Params prm, const __grid_constant__ CUten
         // (head, query block, bias table) of the unit are carried incrementally: this thread is alone on its critical
         // path, and the divisions / modulos of a fresh decomposition cost several hundred cycles per unit
         const int step_h = G / prm.mblocks, step_m = G - step_h * prm.mblocks;
-        int head = (int)blockIdx.x / prm.mblocks, mb = (int)blockIdx.x - head * prm.mblocks;
+        int head = ub0 / prm.mblocks, mb = ub0 - head * prm.mblocks;
         int tab = (a.head0 + head) % a.H;             // head index inside the batch element
         const int step_t = step_h % a.H;
-        for (int u = blockIdx.x; u < prm.units; u += G) {
+        for (int u = ub0; u < prm.units; u += G) {
             const int row0 = mb * BM;
             const int row = row0 + tid;
             const bool row_ok = row < N;
@@ -1167,8 +1169,9 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
         configured[dev] = true;
     }
     const long per_sm = env_long("BA_CTAS_PER_SM", 2);  // dev knob
-    int grid = (int)std::min<long>(prm.units, per_sm * sm_count());
-    if (env_long("BA_GRID", 0) > 0) grid = (int)std::min<long>(prm.units, env_long("BA_GRID", 0));  // dev knob
+    const long count = prm.units - prm.unit0;
+    int grid = (int)std::min<long>(count, per_sm * sm_count());
+    if (env_long("BA_GRID", 0) > 0) grid = (int)std::min<long>(count, env_long("BA_GRID", 0));  // dev knob
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
@@ -1182,7 +1185,7 @@ static int launch_variant(const Params& prm, const Maps& m, cudaStream_t stream)
     // CTAs share an SM: a normal launch places CTA b and b + #SMs together, which pairs a CTA that has one unit more with one
     // that has one less (the survivor then finishes alone, up to 1.8x faster); a programmatic launch fills SMs as K1's CTAs
     // retire and pairs neighbours instead -- measured 7-12% slower at 1024 units (3.46 per CTA), 1-2.6% faster at >= 6.9.
-    const long pdl_default = prm.units >= 6L * grid ? 1 : 0;
+    const long pdl_default = count >= 6L * grid ? 1 : 0;
     cfg.numAttrs = env_long("BA_PDL", pdl_default) ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc_kernel<KPAD, BIAS, MODE, DBG, TL>, prm, m.v, m.b, m.o, m.v16);
     return e == cudaSuccess ? 1 : -(int)e;

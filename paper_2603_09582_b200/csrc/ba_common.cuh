@@ -34,6 +34,7 @@ struct FwdArgs {
     int64_t bias_ld;
     int BH, H, N, d, W64;
     int bias_heads;
+    int unit0, unit1;         // 256-query-row units [unit0, unit1) of THIS call's heads to compute (unit1 == 0: all of them)
     int head0;                // index of this call's first head in the caller's [B*H] grid (bias table = (head0+head) % H % bias_heads)
     int bias_dtype;
     int in_dtype;
@@ -83,5 +84,13 @@ __device__ __forceinline__ float load_as_float(const void* base, int dtype, int6
 }
 
 __host__ __device__ inline int dtype_size(int dtype) { return dtype == BA_F32 ? 4 : 2; }
+
+// Shard units (BA_UNIT_ROWS = 256 query rows) of a call: count per head, and "does the call compute row `row` of head `head`".
+__host__ __device__ inline int units_per_head(int N) { return (N + 255) / 256; }
+__host__ __device__ inline bool row_in_units(const FwdArgs& a, int head, int row) {
+    if (a.unit1 == 0) return true;
+    const int u = head * units_per_head(a.N) + row / 256;
+    return u >= a.unit0 && u < a.unit1;
+}
 
 }  // namespace ba

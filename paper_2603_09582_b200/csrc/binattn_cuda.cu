@@ -115,6 +115,12 @@ int check_params(const ba_params* p, bool need_attention) {
             return fail(BA_ERR_VALIDATION, "bias_dtype must be BA_BF16 or BA_F32");
     }
     if (p->d > 256) return fail(BA_ERR_UNSUPPORTED, "head dim %d > 256 is not supported", p->d);
+    if (p->unit_begin != 0 || p->unit_end != 0) {
+        const int64_t total = (int64_t)p->B * p->H * ba::units_per_head(p->N);
+        if (p->unit_begin < 0 || p->unit_end < p->unit_begin || p->unit_end > total)
+            return fail(BA_ERR_VALIDATION, "unit range [%lld, %lld) outside [0, %lld]", (long long)p->unit_begin,
+                        (long long)p->unit_end, (long long)total);
+    }
     if (p->quantize_pv) {
         const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
         if (bc < 1 || bc > p->N)  // attention.cpp:26-28
@@ -312,6 +318,11 @@ int ba_shard_range(int64_t total, int world, int rank, int64_t* begin, int64_t* 
     return BA_OK;
 }
 
+int ba_shard_units(const ba_params* p, int world, int rank, int64_t* begin, int64_t* end) {
+    if (!p || p->B < 1 || p->H < 1 || p->N < 1) return fail(BA_ERR_SHAPE, "shard_units: params must carry B, H, N >= 1");
+    return ba_shard_range((int64_t)p->B * p->H * ba::units_per_head(p->N), world, rank, begin, end);
+}
+
 int ba_select_kernel(const ba_params* p) {
     if (check_params(p, true) != BA_OK) return -1;
     if (p->quantize_pv) return p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT;
@@ -472,7 +483,7 @@ int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* 
 // that first head.  `ws` holds make_layout(p, heads).total bytes, `tickets` 2*heads zeroed counters.
 static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0, int64_t heads, const void* Q, const void* K,
                      const void* V, const void* bias, float* O, float* row_max, float* row_sum, char* ws,
-                     unsigned int* tickets, cudaStream_t stream, bool prof) {
+                     unsigned int* tickets, cudaStream_t stream, bool prof, int unit0 = 0, int unit1 = 0) {
     const Layout L = make_layout(p, heads);
     ba::FwdArgs a{};
     a.V = V;
@@ -514,6 +525,8 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     a.W64 = L.W64;
     a.bias_heads = p->bias_mode != BA_BIAS_NONE ? p->bias_heads : 1;
     a.head0 = (int)(head0 % p->H);
+    a.unit0 = unit0;
+    a.unit1 = unit1;
     a.in_dtype = p->in_dtype;
     a.inv_tau = p->inv_tau;
 
@@ -583,6 +596,18 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     }
     if ((rc = ensure_tickets(h, 2 * (size_t)L.BH))) return rc;
     const bool prof = h->prof_ev && h->prof_n < h->prof_cap;
+    if (p->unit_end > p->unit_begin) {
+        // unit-sharded call: K1 (and K, V, the scales) for every head the range touches, the attention kernel for the range only
+        const int upb = ba::units_per_head(p->N);
+        const int64_t hb = p->unit_begin / upb, he = (p->unit_end - 1) / upb + 1;
+        const size_t in_head = (size_t)p->N * p->d * ba::dtype_size(p->in_dtype), out_head = (size_t)p->N * p->d * sizeof(float);
+        return fwd_range(h, p, kernel, hb, he - hb, static_cast<const char*>(Q) + hb * in_head, static_cast<const char*>(K) + hb * in_head,
+                         static_cast<const char*>(V) + hb * in_head, bias, reinterpret_cast<float*>(reinterpret_cast<char*>(O) + hb * out_head),
+                         row_max ? row_max + hb * p->N : nullptr, row_sum ? row_sum + hb * p->N : nullptr,
+                         static_cast<char*>(workspace), h->tickets, stream, prof, (int)(p->unit_begin - hb * upb),
+                         (int)(p->unit_end - hb * upb));
+    }
+    if (p->unit_begin != 0 || p->unit_end != 0) return BA_OK;  // empty range
     return fwd_range(h, p, kernel, 0, L.BH, Q, K, V, bias, O, row_max, row_sum, static_cast<char*>(workspace), h->tickets,
                      stream, prof);
 }
@@ -596,6 +621,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     if (rc) return rc;
     if (!Q || !K || !V || !O) return fail(BA_ERR_SHAPE, "attention: Q, K, V and O must be non-NULL");
     if (p->bias_mode != BA_BIAS_NONE && !bias) return fail(BA_ERR_SHAPE, "bias: table / offsets pointer is NULL");
+    if (p->unit_begin != 0 || p->unit_end != 0) return fail(BA_ERR_UNSUPPORTED, "the host-buffer call takes whole batches (no unit range)");
     BA_BIND_DEVICE(h);
     int kernel = 0;
     if ((rc = resolve_kernel(p, &kernel))) return rc;

@@ -42,6 +42,12 @@ def shard_plan(B: int, H: int, world: int, rank: int) -> dict:
     return {"mode": "heads", "begin": b, "end": e}
 
 
+def shard_units(B: int, H: int, N: int, world: int, rank: int) -> tuple[int, int]:
+    """ba_shard_units: contiguous range of the B*H*ceil(N/256) (head, 256-query-row block) units owned by `rank`; pass it to
+    BinaryAttention.forward(..., units=...) on tensors that hold every head the range touches."""
+    return shard_range(B * H * ((N + 255) // 256), world, rank)
+
+
 class ShardedBinaryAttention:
     """Per-GPU launcher for a sharded BinaryAttention forward (see the module docstring)."""
 
@@ -84,6 +90,12 @@ class ShardedBinaryAttention:
             import torch
             return torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
         return self.ba.forward(Q, K, V, bias, scale, kernel=kernel)
+
+    def forward_units(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None):
+        """Unit-sharded forward on the FULL [B,H,N,d] tensors (resident on every rank): this rank computes its (head, 256-row
+        block) units only; rows of other ranks' units stay zero in the returned tensor (sum or gather to combine)."""
+        B, H, N = Q.shape[0], Q.shape[1], Q.shape[2]
+        return self.ba.forward(Q, K, V, bias, scale, kernel=kernel, units=shard_units(B, H, N, self.world, self.rank), out=out)
 
     def gather(self, O_local, B: int, H: int):
         """All ranks' outputs as one [B,H,N,d] tensor (all_gather of equal-size padded shards; verification only)."""

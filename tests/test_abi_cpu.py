@@ -77,6 +77,16 @@ def test_shard_range_matches_python_and_covers(lib):
             assert max(sizes) - min(sizes) <= 1
     b, e = C.c_int64(), C.c_int64()
     assert lib.ba_shard_range(4, 2, 2, C.byref(b), C.byref(e)) == 2  # ValidationError
+    # (head, 256-row block) units: B*H*ceil(N/256) of them, same arithmetic
+    from paper_2603_09582_b200.api import _Params
+    lib.ba_shard_units.argtypes = [C.POINTER(_Params), C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    p = _Params(B=1, H=16, N=4096, d=64)
+    got = []
+    for rank in range(8):
+        assert lib.ba_shard_units(C.byref(p), 8, rank, C.byref(b), C.byref(e)) == 0
+        assert (b.value, e.value) == shard_range(16 * 16, 8, rank)
+        got.append((b.value, e.value))
+    assert got[0][0] == 0 and got[-1][1] == 256 and all(got[i][1] == got[i + 1][0] for i in range(7))
 
 
 def test_reference_error_mirrors():
@@ -117,6 +127,21 @@ bufs = [torch.zeros_like(pad) for _ in range(world)]
 dist.all_gather(bufs, pad)
 full = torch.cat([bufs[r][:, : counts[r]] for r in range(world)], dim=1).reshape(B, H, N, d)
 assert torch.equal(full, x * 2.0 + 1.0), "1-vs-k shard gather mismatch"
+# the launcher class (same plan / gather code bench.py runs under torchrun with NCCL), batch-split and head-split plans
+from paper_2603_09582_b200 import ShardedBinaryAttention, shard_plan, shard_units
+sh = ShardedBinaryAttention(rank, world, 0)
+for (Bb, Hh) in ((4, 3), (1, 5), (3, 5)):
+    xb = torch.arange(Bb * Hh * N * d, dtype=torch.float32).reshape(Bb, Hh, N, d)
+    bias = torch.arange(Hh * N * N, dtype=torch.float32).reshape(Hh, N, N)
+    Ql, Kl, Vl, bl = sh.shard(xb, xb, xb, bias)
+    pl = shard_plan(Bb, Hh, world, rank)
+    assert Ql.shape[0] * Ql.shape[1] == pl["end"] - pl["begin"]
+    if pl["mode"] == "heads" and Ql.shape[1]:  # one bias table per local head, in grid order
+        assert bl.shape[0] == Ql.shape[1] and torch.equal(bl[0], bias[pl["begin"] % Hh])
+    assert torch.equal(sh.gather(Ql * 3.0, Bb, Hh), xb * 3.0)
+# (head, 256-row block) units: the ranks' ranges tile the grid, and a rank's rows are the rows of its units
+ranges = [shard_units(1, 5, 600, world, r) for r in range(world)]
+assert ranges[0][0] == 0 and ranges[-1][1] == 5 * 3 and all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
 t = torch.tensor([float(rank + 1)]); dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max-over-ranks timing reduction
 assert t.item() == world
 dist.barrier(); dist.destroy_process_group()

@@ -177,3 +177,30 @@ def test_run_to_run_identity_stress(ba, B, H, n, d, with_bias, stats):
             first = o.clone()
         else:
             assert torch.equal(o, first)
+
+
+@pytest.mark.parametrize("B,H,n,d,dtype,with_bias", [(2, 3, 1024, 64, "bf16", True), (1, 5, 640, 72, "bf16", False), (2, 3, 300, 64, "bf16", True),
+                                                     (3, 2, 197, 64, "bf16", True), (1, 3, 300, 40, "f32", True), (1, 2, 1536, 128, "bf16", True)])
+def test_unit_shards_reproduce_the_full_run(ba, B, H, n, d, dtype, with_bias):
+    """(head, 256-row block) shards (ba_shard_units -> ba_params.unit_begin / unit_end) written into one
+    output buffer by 3, 5 and 7 'ranks' give the full run byte for byte -- ranges that split heads, both tcgen05 kernels
+    (N = 300: three 128-row blocks in two shard units) and the CUDA-core kernel."""
+    import torch
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    g = torch.Generator(device="cuda").manual_seed(12)
+    Q, K, V = (torch.randn(B, H, n, d, device="cuda", generator=g).to(tdt) for _ in range(3))
+    bias = None
+    if with_bias:
+        bias = (0.5 * torch.randn(H, n, (n + 7) // 8 * 8, device="cuda", generator=g)).to(torch.bfloat16 if dtype == "bf16" else torch.float32)[:, :, :n]
+    full = ba.forward(Q, K, V, bias)
+    total = B * H * ((n + 255) // 256)
+    for world in (3, 5, 7):
+        out = torch.full_like(full, float("nan"))
+        covered = 0
+        for r in range(world):
+            b, e = ba.shard_units(B, H, n, world, r)
+            covered += e - b
+            ba.forward(Q, K, V, bias, units=(b, e), out=out)
+        torch.cuda.synchronize()
+        assert covered == total
+        assert torch.equal(out, full), f"world {world}"
