@@ -31,6 +31,7 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
         if (a.bias_kind != BA_BIAS_DENSE) return 0;
         const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 && reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         if (!tma_ok) return 0;
+        if (a.N < env_long("BA_TC2_MIN_N_BIAS", 2048)) return 0;  // with a dense bias the first-generation kernel is level or ahead below ~2048 keys (measured)
         bias_mode = 1;
     }
     tc::EncodeTiledFn enc = tc::get_encode_fn();
@@ -58,14 +59,19 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     prm.vst = 4;
     prm.qst = 2;
     prm.bst = bias_mode == 1 ? 6 : 0;
+    // the staged (TMA store) epilogue matters when units are short; long units (>= 64 key tiles) keep their deeper rings instead
+    prm.o_stage = (env_long("BA_O_STAGE", 1) && prm.tiles < 64) ? 1 : 0;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.kst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 5) prm.bst = 5;
+    if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.o_stage) prm.vst = 3;
+    if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.o_stage && prm.bst > 4) prm.bst = 4;
+    if (smem_bytes2(prm, kpad) > kSmemMax2) prm.o_stage = 0;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.qst = 1;
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.vst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 4) prm.bst = 4;
     if (smem_bytes2(prm, kpad) > kSmemMax2) return 0;
 
-    CUtensorMap vmap, bmap;
+    CUtensorMap vmap, bmap, omap;
     const cuuint32_t estr[3] = {1, 1, 1};
     {
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
@@ -74,6 +80,14 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
         if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.V), gdim, gstr, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    }
+    {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 16 floats (64 B, 64B swizzle), clipped at N and d by the hardware
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
+        const cuuint32_t box[3] = {16, 32, 1};
+        if (enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
     bmap = vmap;
@@ -87,10 +101,10 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
             return -(int)cudaErrorInvalidValue;
     }
     switch (kpad) {
-        case 32: return launch_kpad2<32>(prm, bias_mode, vmap, bmap, stream);
-        case 64: return launch_kpad2<64>(prm, bias_mode, vmap, bmap, stream);
-        case 96: return launch_kpad2<96>(prm, bias_mode, vmap, bmap, stream);
-        case 128: return launch_kpad2<128>(prm, bias_mode, vmap, bmap, stream);
+        case 32: return launch_kpad2<32>(prm, bias_mode, vmap, bmap, omap, stream);
+        case 64: return launch_kpad2<64>(prm, bias_mode, vmap, bmap, omap, stream);
+        case 96: return launch_kpad2<96>(prm, bias_mode, vmap, bmap, omap, stream);
+        case 128: return launch_kpad2<128>(prm, bias_mode, vmap, bmap, omap, stream);
     }
     return 0;
 }

@@ -42,6 +42,7 @@ constexpr int TN = 64;             // keys per tile (UMMA N of the S MMA)
 constexpr int kThreads2 = 640;
 constexpr int kColO2 = 256;        // first O column; tile X owns [256 + 128 X, +dvp)
 constexpr int kVBox = 8192;        // one TMA box of V: 64 keys x 64 columns bf16, 128B swizzle
+constexpr int kOStage = 16 * 2048;  // epilogue staging: 16 warps x one 2 KB box ([32 rows][16 floats], 64B swizzle)
 constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16, 128B swizzle
 #ifndef BA_PP_AT
 #define BA_PP_AT -1  // (measured: no gain with mbarriers or named barriers; kept as a dev knob) exponent pair after which a warp hands the MUFU pipe to the other query tile's pair (-1: no ping-pong)
@@ -77,6 +78,7 @@ struct Params2 {
     int dvp;       // d rounded up to 16
     int nbox;      // ceil(d / 64) TMA boxes per V tile
     int qst, kst, vst, bst;
+    int o_stage;   // the epilogue goes through per-warp staging boxes and TMA stores (when 32 KB of shared memory are left)
     int g;         // BIAS 4: grid side sqrt(N) (a multiple of 32)
     int32_t* dbg_S;
     int dbg_head;
@@ -107,13 +109,14 @@ __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 6
 template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
 __global__ void __launch_bounds__(kThreads2, 1)
 attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUtensorMap vmap,
-                const __grid_constant__ CUtensorMap bmap) {
+                const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
     unsigned char* sV = smem_raw;                               // vst x nbox x 8 KB
     unsigned char* sB = sV + prm.vst * prm.nbox * kVBox;        // bst x 16 KB
     unsigned char* sQ = sB + prm.bst * kBSub;                   // qst x 256 x KPAD (tile A rows, then tile B rows)
-    unsigned char* sK = sQ + prm.qst * 2 * TM * KPAD;           // kst x 64 x KPAD
+    unsigned char* sO = sQ + prm.qst * 2 * TM * KPAD;           // o_stage x 16 x 2 KB: one [32 rows][16 floats] staging box per softmax warp
+    unsigned char* sK = sO + prm.o_stage * kOStage;             // kst x 64 x KPAD
     Smem2* sm = reinterpret_cast<Smem2*>(sK + prm.kst * TN * KPAD);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -158,6 +161,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
     if (warp == 18 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
         if (BIAS == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+        if (prm.o_stage) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&omap)) : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -355,6 +359,13 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const int nlast = N - (T - 1) * TN;  // keys of the last tile (TN unless N is ragged)
         uint32_t gx = 0;  // key tiles this query tile has been through (stage = gx & 1, parity = (gx >> 1) & 1)
         int usm = -1;     // units of this CTA so far (slot of the BIAS 4 tables)
+        // per-head scales are requested one unit ahead (a fresh global load costs this in-order thread ~700 clk per unit)
+        float muq_n = 0.f, muk_n = 0.f;
+        if (ub0 < prm.units) {
+            muq_n = __ldg(a.mu_q + ub0 / prm.ublocks);
+            muk_n = __ldg(a.mu_k + ub0 / prm.ublocks);
+        }
+        unsigned char* box = sO + warp * 2048;  // my warp's staging box (o_stage)
         uint32_t np = 0;  // tiles done in ping-pong with the other query tile
         Ring br;          // position of my query tile's next bias tile in the producer's ring
         if (BIAS == 1 && X == 1) br.next(prm.bst);
@@ -370,7 +381,11 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             }
             const bool pp = nact == 2 && BA_PP_AT >= 0;
             const int row = ub * 2 * TM + X * TM + r;
-            const float sc = __ldg(a.mu_q + head) * __ldg(a.mu_k + head) * a.inv_tau;  // natural-log units per unit of dot
+            const float sc = muq_n * muk_n * a.inv_tau;  // natural-log units per unit of dot
+            if (u + G < prm.units) {
+                muq_n = __ldg(a.mu_q + (u + G) / prm.ublocks);
+                muk_n = __ldg(a.mu_k + (u + G) / prm.ublocks);
+            }
             const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;  // BIAS 0 keeps x = raw dot and folds the scale into the exponent
             const bool fast = BIAS == 0 && !stats && !DBG && sc * kLog2e * (float)d <= kFastBound;
             float m_ref = fast ? sc * kLog2e * (float)d : -INFINITY, m_true = -INFINITY;
@@ -512,10 +527,28 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             for (int c = oc0; c < oc1; c += 16) {
                 float o[16];
                 BA_TMEM_LD16(o_addr + c, o, 0);
+                if (prm.o_stage) {  // the box is free again once the TMA unit has READ the previous chunk out of it
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                }
                 tc_wait_ld();
 #pragma unroll
                 for (int i = 0; i < 16; ++i) o[i] *= inv_l;
-                if (row < N) {
+                if (prm.o_stage) {
+                    // Direct stores (32 lanes x 32 B to 32 different rows per instruction) keep the LSU busy for ~2000 clk per
+                    // unit; a [32 rows][16 floats] box in shared memory (64B swizzle: 16-byte chunk q of row r sits at
+                    // q ^ ((r >> 1) & 3)) goes out as ONE asynchronous TMA store, clipped at N and d by the hardware.
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        *reinterpret_cast<float4*>(box + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&omap, box, c, row - lane, head);
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else if (row < N) {
                     if (c + 8 <= d) stg_256(orow + c, o);
                     if (c + 16 <= d) stg_256(orow + c + 8, o + 8);
                 }
@@ -527,6 +560,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             }
             warp_arrive(&sm->ofree[X], lane);
         }
+        if (prm.o_stage && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory may be released
     }
     tc_fence_before();
     __syncthreads();
@@ -546,7 +580,8 @@ template <int KPAD>
 __global__ void __launch_bounds__(256) expand_qk_kernel(const uint64_t* __restrict__ q_words, const uint64_t* __restrict__ k_words,
                                                         unsigned char* __restrict__ q_out, unsigned char* __restrict__ k_out,
                                                         int64_t heads, int N, int ktiles, int qtiles, int w64, int d) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the attention kernel's prologue may start
+    asm volatile("griddepcontrol.wait;" ::: "memory");               // K1's packed words are read from here on
     constexpr int C = KPAD / 16;
     const bool isq = blockIdx.y == 1;
     const int R = isq ? 128 : 64, sh = isq ? 7 : 6, tiles = isq ? qtiles : ktiles;
@@ -569,10 +604,17 @@ __global__ void __launch_bounds__(256) expand_qk_kernel(const uint64_t* __restri
 template <int KPAD>
 static int launch_expand_qk(const FwdArgs& a, int ktiles, int ublocks, cudaStream_t stream) {
     const int64_t qchunks = (int64_t)a.BH * ublocks * 2 * (KPAD / 16) * 128;  // >= the K plane's chunk count
-    dim3 grid((unsigned)((qchunks + 255) / 256), 2);
-    expand_qk_kernel<KPAD><<<grid, 256, 0, stream>>>(a.q_words, a.k_words, const_cast<unsigned char*>(a.q_exp),
-                                                     const_cast<unsigned char*>(a.k_exp), a.BH, a.N, ktiles, 2 * ublocks, a.W64, a.d);
-    const cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((qchunks + 255) / 256), 2);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // launch latency hides behind K1 (which releases its
+    attr[0].val.programmaticStreamSerializationAllowed = 1;           // dependents on entry); the data wait is in the kernel
+    cfg.attrs = attr;
+    cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, expand_qk_kernel<KPAD>, a.q_words, a.k_words, const_cast<unsigned char*>(a.q_exp),
+                                             const_cast<unsigned char*>(a.k_exp), (int64_t)a.BH, a.N, ktiles, 2 * ublocks, a.W64, a.d);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
@@ -580,11 +622,11 @@ constexpr size_t kSmemMax2 = 227 * 1024;
 
 inline size_t smem_bytes2(const Params2& p, int kpad) {
     return (size_t)p.vst * p.nbox * kVBox + (size_t)p.bst * kBSub + (size_t)p.qst * 2 * TM * kpad + (size_t)p.kst * TN * kpad +
-           sizeof(Smem2);
+           (size_t)p.o_stage * kOStage + sizeof(Smem2);
 }
 
 template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
-static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
     static bool configured[kMaxDevices] = {};
     const int dev = current_device();
     if (!configured[dev]) {
@@ -605,35 +647,35 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, prm, vmap, bmap);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, prm, vmap, bmap, omap);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
 template <int KPAD>
-static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream);
+static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream);
 
 template <int KPAD>
-static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+static int launch_kpad2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
     const int ne = launch_expand_qk<KPAD>(prm.a, prm.tiles, prm.ublocks, stream);
     if (ne < 0) return ne;
-    const int nk = launch_main2<KPAD>(prm, bias_mode, vmap, bmap, stream);
+    const int nk = launch_main2<KPAD>(prm, bias_mode, vmap, bmap, omap, stream);
     return nk < 0 ? nk : ne + nk;
 }
 
 template <int KPAD>
-static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, cudaStream_t stream) {
+static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
     if (prm.dbg_T && bias_mode == 0 && (KPAD == 64 || KPAD == 128)) {
-        if (prm.a.N % TN != 0 && KPAD == 64) return launch_variant2<KPAD, 0, false, true, true>(prm, vmap, bmap, stream);
-        return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, stream);
+        if (prm.a.N % TN != 0 && KPAD == 64) return launch_variant2<KPAD, 0, false, true, true>(prm, vmap, bmap, omap, stream);
+        return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, omap, stream);
     }
-    if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, stream);
-    if (bias_mode == 4) return launch_variant2<KPAD, 4, false>(prm, vmap, bmap, stream);
+    if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, omap, stream);
+    if (bias_mode == 4) return launch_variant2<KPAD, 4, false>(prm, vmap, bmap, omap, stream);
     if (prm.a.N % TN != 0) {
-        if (bias_mode == 1) return launch_variant2<KPAD, 1, false, false, true>(prm, vmap, bmap, stream);
-        return launch_variant2<KPAD, 0, false, false, true>(prm, vmap, bmap, stream);
+        if (bias_mode == 1) return launch_variant2<KPAD, 1, false, false, true>(prm, vmap, bmap, omap, stream);
+        return launch_variant2<KPAD, 0, false, false, true>(prm, vmap, bmap, omap, stream);
     }
-    if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, stream);
-    return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, stream);
+    if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, omap, stream);
+    return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, omap, stream);
 }
 
 }  // namespace tc2
