@@ -423,11 +423,12 @@ def test_relative_2d_bias(ba, port, n, d, g):
         ba.forward(Q[:, :, :200], K[:, :, :200], V[:, :, :200], rel)
 
 
-def test_relative_2d_bias_in_kernel_bit_identical(ba, port):
+def test_relative_2d_bias_in_kernel_bit_identical(ba, port, monkeypatch):
     """In-kernel generation vs the same kernel's dense path fed materialize_bias' table: bit-identical when every sum
     row + col is bf16-representable (offsets on a 1/8 grid), per-head tables, bf16 and fp32 offsets."""
     import torch
     import paper_2603_09582_b200 as pkg
+    monkeypatch.setenv("BA_TC2_MIN_N_BIAS", "512")  # the dense call must run on the second-generation kernel too (dev knob)
     B, H, n, d, g = 2, 3, 1024, 64, 32
     gen = torch.Generator(device="cuda").manual_seed(44)
     Q, K, V = (torch.randn(B, H, n, d, device="cuda", generator=gen).to(torch.bfloat16) for _ in range(3))
