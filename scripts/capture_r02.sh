@@ -1,0 +1,21 @@
+#!/bin/bash
+# Round-2 evidence capture on one B200 (run under gpurun): bench lines, ncu summaries of the final build, launch list, sanitizer.
+set -x
+mkdir -p gpurun_out
+python bench.py > gpurun_out/r02_bench_default.json 2> gpurun_out/r02_bench_default.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r02_bench_reference_arm.json 2> gpurun_out/r02_bench_reference_arm.err
+python bench.py --workload c2 --no-sweep > gpurun_out/r02_bench_c2.json 2>> gpurun_out/r02_bench_default.err
+python bench.py --workload c4 --no-sweep > gpurun_out/r02_bench_c4.json 2>> gpurun_out/r02_bench_default.err
+NCU="ncu --set full --clock-control none --import-source on -s 2 -c 1"
+$NCU -k regex:attn_tc2 -o gpurun_out/r02_c5_16384_128_bias python scripts/run_one.py 1 16 16384 128 1 3 > gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc2 -o gpurun_out/r02_c5_16384_128_nobias python scripts/run_one.py 1 16 16384 128 0 3 >> gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc2 -o gpurun_out/r02_c5_16384_64_nobias python scripts/run_one.py 1 16 16384 64 0 3 >> gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc2 -o gpurun_out/r02_c5_4096_64_nobias python scripts/run_one.py 1 16 4096 64 0 3 >> gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc2 -o gpurun_out/r02_c4_nobias python scripts/run_one.py 32 16 1024 72 0 3 >> gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc_kernel -o gpurun_out/r02_c4_bias python scripts/run_one.py 32 16 1024 72 1 3 >> gpurun_out/ncu.log 2>&1
+$NCU -k regex:attn_tc_kernel -o gpurun_out/r02_c2_bias python scripts/run_one.py 256 12 197 64 1 3 >> gpurun_out/ncu.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r02_launches_default.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu-baseline > /dev/null 2>&1
+timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_tc2.py -q -m gpu -k "matches_oracle or logits or unit_shards or fast_path" > gpurun_out/r02_sanitizer_memcheck.txt 2>&1
+tail -5 gpurun_out/r02_sanitizer_memcheck.txt
+python scripts/peakedness_table.py > gpurun_out/r02_peakedness.md 2>&1
+ls -la gpurun_out | tail -20
