@@ -328,6 +328,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--quick-sweep", action="store_true", help="sweep only the first four shapes")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 -> min(steps, 3 for the 8.6 GB bias workloads, else 10)")
+    ap.add_argument("--single-device", action="store_true",
+                    help="dev: every rank uses cuda:0 and the gloo backend, to walk the sharded path on a one-GPU box")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     B, H, N, d, desc = WORKLOADS[args.workload]
@@ -347,15 +349,23 @@ def main():
     if not torch.cuda.is_available():
         print(json.dumps({"error": "no CUDA device; this benchmark has no CPU fallback"}))
         return 1
+    if args.single_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=device)
+        if args.single_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if args.single_device:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
     sh = pkg.ShardedBinaryAttention(rank, world, local_rank, device)
@@ -418,7 +428,7 @@ def main():
             Oone = ba.forward(Qf, Kf, Vf, biasf, kernel=kernel)
             torch.cuda.synchronize()
             verify = {"gathered_equals_one_gpu_run": bool(torch.equal(Og, Oone)), "bytes": Og.numel() * 4,
-                      "collective": "NCCL all_gather of O, outside the timed region"}
+                      "collective": ("gloo" if args.single_device else "NCCL") + " all_gather of O, outside the timed region"}
             del Oone
         del Og
 
