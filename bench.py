@@ -315,6 +315,62 @@ def run_sweep(ba, device, index, quick=False):
 
 
 # --------------------------------------------------------------------------------------------- main
+def measure_traffic(args, kernel):
+    """DRAM bytes of ONE launch of the K2 kernel(s) on this workload, measured now: a child copy of this script
+    (--traffic-probe: the same inputs, one forward) runs under `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum`
+    after every timed region has ended.  Only byte counters are read from the profiled run, never a time."""
+    import csv
+    import shutil
+    import subprocess
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found on this box"
+    if os.environ.get("CUDA_INJECTION64_PATH") or os.environ.get("NV_COMPUTE_PROFILER_PERFWORKS_DIR"):
+        return None, "this run is itself under a profiler"
+    with tempfile.TemporaryDirectory() as tmp:
+        log = os.path.join(tmp, "traffic.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--print-units", "base",
+               "--csv", "--log-file", log, "-k", "regex:attn_tc|expand_qk|expand_rel2d", sys.executable, os.path.abspath(__file__),
+               "--traffic-probe", "--workload", args.workload, "--kernel", kernel] + (["--no-bias"] if args.no_bias else [])
+        try:
+            r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, timeout=420, text=True)
+        except subprocess.TimeoutExpired:
+            return None, "ncu probe timed out"
+        if r.returncode != 0 or not os.path.exists(log):
+            return None, "ncu probe failed: " + (r.stdout or "")[-160:].replace("\n", " ")
+        per_kernel, total = {}, 0.0
+        with open(log, newline="") as f:
+            rows = [row for row in csv.reader(f) if row and row[0] not in ("", ) and not row[0].startswith("==")]
+        head = next((r_ for r_ in rows if "Metric Name" in r_), None)
+        if head is None:
+            return None, "ncu probe: no metric rows"
+        ik, im, iv = head.index("Kernel Name"), head.index("Metric Name"), head.index("Metric Value")
+        for row in rows:
+            if len(row) <= iv or row[im] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                continue
+            v = float(row[iv].replace(",", ""))
+            name = row[ik].split("(")[0].split("<")[0].split()[-1]
+            per_kernel.setdefault(name, {"dram__bytes_read.sum": 0.0, "dram__bytes_write.sum": 0.0})[row[im]] += v
+            total += v
+        if not per_kernel:
+            return None, "ncu probe: no K2 launch seen"
+        return total, {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum on one forward of this workload in a child "
+                              "process after the timed regions (cold caches, as ncu replays it)", "per_kernel": per_kernel}
+
+
+def traffic_probe(args, B, H, N, d):
+    """Child of measure_traffic: the workload's inputs, ONE forward, nothing printed."""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    device = torch.device("cuda", 0)
+    ba = pkg.BinaryAttention(device)
+    Q, K, V, bias = make_inputs(B, H, N, d, device, seed=1234)
+    ba.forward(Q, K, V, None if args.no_bias else bias, kernel=args.kernel)
+    torch.cuda.synchronize()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,9 +386,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 -> min(steps, 3 for the 8.6 GB bias workloads, else 10)")
     ap.add_argument("--single-device", action="store_true",
                     help="dev: every rank uses cuda:0 and the gloo backend, to walk the sharded path on a one-GPU box")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-bytes probe (roofline.traffic = null)")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     B, H, N, d, desc = WORKLOADS[args.workload]
+    if args.traffic_probe:
+        return traffic_probe(args, B, H, N, d)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -484,8 +544,8 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_sustained"]}
     roof.update({"traffic": None,
-                 "traffic_note": "not measured in this run (needs ncu); the ncu --set full captures of this build are under "
-                                 "profiles/ (r02_*), DRAM bytes per launch in their summaries",
+                 "traffic_note": "not measured (--no-traffic or N > 1); ncu --set full captures of this build are under profiles/ "
+                                 "(r02_*), DRAM bytes per launch in their summaries",
                  "kernel": f"K2 fused attention ({used}; includes the K-plane expansion launch where the second-generation "
                            "kernel runs)", "kernel_ms": k2_ms,
                  "algorithmic_bytes": k2_bytes, "peak_source": pk["source"],
@@ -513,6 +573,15 @@ def main():
         for e in sweep:
             if (e["B"], e["H"], e["N"], e["d"]) == (B, H, N, d) and (e["bias"] is not None) == (not args.no_bias):
                 this = e
+    if not args.no_traffic and world == 1:
+        Q = K = V = bias = O = Qf = Kf = Vf = biasf = None
+        torch.cuda.empty_cache()
+        try:
+            roof["traffic"], roof["traffic_note"] = measure_traffic(args, kernel)
+        except Exception as ex:  # noqa: BLE001
+            roof["traffic"], roof["traffic_note"] = None, f"ncu probe failed: {str(ex)[:160]}"
+        if roof["traffic"]:
+            roof["traffic_over_algorithmic"] = roof["traffic"] / k2_bytes
     cpu = None
     if not args.no_cpu_baseline:
         try:

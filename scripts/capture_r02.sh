@@ -14,7 +14,7 @@ $NCU -k regex:attn_tc2 -o gpurun_out/r02_c5_4096_64_nobias python scripts/run_on
 $NCU -k regex:attn_tc2 -o gpurun_out/r02_c4_nobias python scripts/run_one.py 32 16 1024 72 0 3 >> gpurun_out/ncu.log 2>&1
 $NCU -k regex:attn_tc_kernel -o gpurun_out/r02_c4_bias python scripts/run_one.py 32 16 1024 72 1 3 >> gpurun_out/ncu.log 2>&1
 $NCU -k regex:attn_tc_kernel -o gpurun_out/r02_c2_bias python scripts/run_one.py 256 12 197 64 1 3 >> gpurun_out/ncu.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r02_launches_default.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu-baseline > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r02_launches_default.csv python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu-baseline --no-traffic > /dev/null 2>&1
 timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_tc2.py -q -m gpu -k "matches_oracle or logits or unit_shards or fast_path" > gpurun_out/r02_sanitizer_memcheck.txt 2>&1
 tail -5 gpurun_out/r02_sanitizer_memcheck.txt
 python scripts/peakedness_table.py > gpurun_out/r02_peakedness.md 2>&1

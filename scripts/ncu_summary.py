@@ -27,8 +27,10 @@ for r in rows[2:]:
     for k in KEYS:
         if k in hdr:
             print(f"  {k:72s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
-    dr, dw = float(r[hdr.index('dram__bytes_read.sum')]), float(r[hdr.index('dram__bytes_write.sum')])
-    print(f"  {'traffic = dram read + write':72s} {dr + dw:16.3f} {units[hdr.index('dram__bytes_read.sum')]} (+{units[hdr.index('dram__bytes_write.sum')]})")
+    mult = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = sum(float(r[hdr.index(k)].replace(",", "")) * mult.get(units[hdr.index(k)], 1.0)
+              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    print(f"  {'traffic = dram read + write':72s} {tot / 1e6:16.3f} Mbyte")
 src = list(csv.reader(io.StringIO(run(["--page", "source", "--csv"]))))
 if len(src) > 2:
     h = src[1]
