@@ -96,7 +96,10 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
         const cuuint64_t gstr[2] = {(cuuint64_t)a.bias_ld * 2, (cuuint64_t)a.N * a.bias_ld * 2};
         const cuuint32_t box[3] = {64, (cuuint32_t)TM, 1};
         if (enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.bias), gdim, gstr, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                // 256-byte L2 promotion: a tile row is 128 B of a 2N-byte table row, and the next key tile reads the 128 B beside it --
+                // fetching both at once halves the DRAM page activations of the N x N stream (measured 1-5% on the whole kernel)
+                env_long("BA_BIAS_L2", 256) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }

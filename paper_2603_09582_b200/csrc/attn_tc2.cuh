@@ -98,9 +98,34 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                  : "memory");
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+// Per-thread constants of the softmax loop (addresses derived from %tid) are passed through this so that they live in a
+// register: left alone, the compiler re-derives them from %tid in every key tile (a dozen S2R + ~40 integer instructions
+// per tile in a loop whose issue slots are the bound).
+__device__ __forceinline__ uint32_t keep_u32(uint32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32_volatile(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32_volatile(uint32_t addr, uint32_t v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // BIAS: 0 = none, 1 = dense bf16 table staged by TMA, 4 = Relative2dBias generated from its two offset tables (see below).  Any N >= 128: the K plane is zero-padded to whole 64-key tiles, V and bias
 // tiles are zero-filled past N by the TMA unit, and the last tile's surplus columns are masked to -inf before the row max.
+#ifdef BA_DEV_TL_MMA  // dev builds only: extra stamps inside the elected S-issue block (scripts/timeline_tc2.py ... mma8)
+#define BA_STAMP3() BA_STAMP2()
+#else
+#define BA_STAMP3() do { } while (0)
+#endif
 #define BA_STAMP2()                                                      \
     do {                                                                 \
         if (TL && tl_buf && tl_n < kTlStamps) tl_buf[tl_n++] = clock64(); \
@@ -215,13 +240,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         tc_fence_after();
                         const uint64_t kd = k_desc + (uint64_t)((kr.stage * TN * KPAD) >> 4);
                         if (elect_one()) {
+                            BA_STAMP3();
 #pragma unroll
                             for (int ks = 0; ks < KPAD / 32; ++ks)
                                 mma_f8(s_tmem + (g & 1u) * TN, qd + (uint64_t)(ks * ((2 * TM * 16) >> 4)),
                                        kd + (uint64_t)(ks * ((2 * TN * 16) >> 4)), idesc_s, ks > 0 ? 1u : 0u);
+                            BA_STAMP3();
                             tc_commit(&sm->sfull[X][g & 1u]);
+                            BA_STAMP3();
                             tc_commit(&sm->kfree[kr.stage]);
                             if (j == T - 1) tc_commit(&sm->qfree[qr.stage]);
+                            BA_STAMP3();
                         }
                         __syncwarp();
                     } else if (lane == 0) {
@@ -350,7 +379,12 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const int X = warp >> 3, half = (warp >> 2) & 1, quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-        const uint32_t s_base = lane_base + X * 128 + half * 32;  // + 64 * stage: my 32 S columns; P goes over the first 16
+        const uint32_t s_base = keep_u32(lane_base + X * 128 + half * 32);  // + 64 * stage: my 32 S columns; P goes over the first 16
+        // my row of a bias tile: 16-byte chunk (half*4 + c) ^ (r & 7) of row r = (this address) ^ (c << 4) (+ the stage offset;
+        // the ring is 1024-byte aligned)
+        const uint32_t b_thr = keep_u32(smem_u32(sB) + r * 128 + ((((uint32_t)half << 2) ^ (uint32_t)(r & 7)) << 4));
+        const uint32_t fl_thr = keep_u32(smem_u32(&sm->flag[0][X][quad][0]));  // + (gx & 1) * sizeof(flag[0]); [half] = mine
+        const uint32_t lane0 = keep_u32(lane == 0 ? 1u : 0u);
         const uint32_t o_addr = lane_base + kColO2 + X * 128;
         const int pair_id = 1 + X * 4 + quad;
         const int h16 = ((prm.dvp >> 1) + 15) & ~15;             // O columns [0,h16) belong to half 0, [h16,dvp) to half 1
@@ -418,17 +452,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         if (row < N && j * TN + half * 32 + i < N) drow[i] = (int)x[i];
                 }
                 if (BIAS == 1) {
-                    const unsigned char* brow = sB + br.stage * kBSub + r * 128;  // row r of the 128 x 64 bf16 tile
+                    const uint32_t brow = b_thr + br.stage * kBSub;  // row r of the 128 x 64 bf16 tile, my half's first chunk
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        const uint4 b = *reinterpret_cast<const uint4*>(brow + (((half * 4 + c) ^ (r & 7)) << 4));
+                        const uint4 b = lds_128(brow ^ (c << 4));
                         const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
                             fma2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], sc, sc,
                                  __uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xFFFF0000u));
                     }
-                    warp_arrive(&sm->bfree[br.stage], lane);
+                    warp_arrive(&sm->bfree[br.stage], (int)(lane0 ^ 1u));
                     br.next(prm.bst);  // tile A and tile B alternate in the ring when both are active
                     if (nact == 2) br.next(prm.bst);
                 }
@@ -461,10 +495,10 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     const float hm = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * ea;  // ea > 0: the max commutes with the scaling
                     const bool need = hm > m_ref + kThr2;
                     const uint32_t mine = (stats || __any_sync(0xffffffffu, need)) ? 1u : 0u;
-                    volatile uint32_t* fl = &sm->flag[gx & 1u][X][quad][0];
-                    if (lane == 0) fl[half] = mine;
+                    const uint32_t fl = fl_thr + (gx & 1u) * (uint32_t)sizeof(sm->flag[0]);
+                    if (lane0) sts_u32_volatile(fl + half * 4, mine);
                     pair_sync(pair_id);
-                    if (mine | fl[half ^ 1]) {  // rare after the first tile of a unit: agree on a new reference for the rows that need one
+                    if (mine | lds_u32_volatile(fl + (half ^ 1) * 4)) {  // rare after the first tile of a unit: agree on a new reference for the rows that need one
                         sm->xch[X][half][r] = hm;
                         pair_sync(pair_id);
                         const float tm = fmaxf(hm, sm->xch[X][half ^ 1][r]);
@@ -514,7 +548,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 BA_STAMP2();
                 tc_wait_st();
                 tc_fence_before();
-                warp_arrive(&sm->pfull[X][st], lane);
+                warp_arrive(&sm->pfull[X][st], (int)(lane0 ^ 1u));
             }
             // ---------------------------------------------------------------- epilogue: O / l for my half of the columns
             mbar_wait(&sm->pvdone[X][(gx - 1) & 1u], ((gx - 1) >> 1) & 1u);
@@ -668,6 +702,9 @@ static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vm
         if (prm.a.N % TN != 0 && KPAD == 64) return launch_variant2<KPAD, 0, false, true, true>(prm, vmap, bmap, omap, stream);
         return launch_variant2<KPAD, 0, false, true>(prm, vmap, bmap, omap, stream);
     }
+#ifdef BA_DEV_TL_BIAS  // dev builds only: clock64 timeline of the dense-bias variant (scripts/timeline_tc2.py)
+    if (prm.dbg_T && bias_mode == 1 && KPAD == 128 && prm.a.N % TN == 0) return launch_variant2<KPAD, 1, false, true>(prm, vmap, bmap, omap, stream);
+#endif
     if (prm.dbg_S && bias_mode == 0) return launch_variant2<KPAD, 0, true>(prm, vmap, bmap, omap, stream);
     if (bias_mode == 4) return launch_variant2<KPAD, 4, false>(prm, vmap, bmap, omap, stream);
     if (prm.a.N % TN != 0) {
