@@ -93,6 +93,10 @@ typedef struct {
                             (b, h, BA_UNIT_ROWS-row block) grid -- B*H*ceil(N/BA_UNIT_ROWS) units, see ba_shard_units -- and leaves
                             every other row of O / row_max / row_sum untouched.  A range may split a head: K, V and the
                             per-head scales of every head it touches are still processed whole.  0, 0 = all units. */
+    int32_t out_bf16;    /* 0: O is float32 (AttentionOutput::output, attention.hpp:44).  1: O is written as bfloat16
+                            [B,H,N,d] -- the fp32 result rounded to nearest-even in the kernel's epilogue, i.e. exactly
+                            what converting the fp32 output afterwards gives, without the fp32 round trip through HBM.
+                            The O argument then points to bf16 storage.  row_max / row_sum stay float32. */
 } ba_params;
 
 #define BA_UNIT_ROWS 256 /* query rows of one shard unit (one unit of the second-generation kernel, two of the first's) */
@@ -148,14 +152,14 @@ int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* 
  * row_max / row_sum: optional [B,H,N] float32 (AttentionOutput::row_max / row_sum, attention.hpp:45-46).
  * quantize_pv = 1 selects the reference's integer P.V mode (attention.cpp:332-343, 361-363). */
 int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
-                            const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
+                            const void* bias, void* O, float* row_max, float* row_sum, void* workspace,
                             void* stream);
 
 /* Same call with HOST buffers (what a reference-side binding uses): copies Q,K,V(,bias) to the device,
  * runs ba_binary_attention_fwd, copies O (and row_max/row_sum when non-NULL) back, and synchronises.
  * Device staging buffers are owned and cached by the handle.  Pinned host memory makes the copies async. */
 int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
-                             const void* bias, float* O, float* row_max, float* row_sum);
+                             const void* bias, void* O, float* row_max, float* row_sum);
 
 /* Launcher partition: contiguous range of the flattened B*H head grid owned by
  * `rank` of `world` single-GPU processes.  No collective is needed on the hot path. */

@@ -52,7 +52,8 @@ class _Params(C.Structure):
     _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("N", C.c_int32), ("d", C.c_int32), ("in_dtype", C.c_int32),
                 ("bias_mode", C.c_int32), ("bias_heads", C.c_int32), ("bias_dtype", C.c_int32),
                 ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32),
-                ("quantize_pv", C.c_int32), ("block_cols", C.c_int32), ("unit_begin", C.c_int64), ("unit_end", C.c_int64)]
+                ("quantize_pv", C.c_int32), ("block_cols", C.c_int32), ("unit_begin", C.c_int64), ("unit_end", C.c_int64),
+                ("out_bf16", C.c_int32)]
 
 
 _lib = None
@@ -353,8 +354,10 @@ class BinaryAttention:
         return FidelityReport(out.cos_sim, out.relative_l1, out.rmse, out.precision_at_k, int(k))
 
     def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", return_stats=False, quantize_pv=False, block_cols=None,
-                units=None, out=None):
-        """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors (fp32 output).
+                units=None, out=None, out_dtype=torch.float32):
+        """binary_attention(Q, K, V, bias, scale) -> O for [B,H,N,d] device tensors.  O is float32 like the reference's
+        output; out_dtype=torch.bfloat16 (ba_params.out_bf16) has the kernel's epilogue write the same values rounded to
+        bfloat16 (nearest-even) instead -- bit-identical to forward(...).to(torch.bfloat16), half the output bytes.
         quantize_pv=True selects the reference's default u8 x s8 integer P.V mode (attention.hpp:35; CUDA-core kernel);
         block_cols is that mode's key-block size (default min(64, N), like AttentionConfig::make).
         units=(begin, end): compute only those (head, 256-row block) units of the flattened grid (ba_shard_units); the other
@@ -375,12 +378,15 @@ class BinaryAttention:
             p.unit_begin, p.unit_end = int(units[0]), int(units[1])
             if p.unit_begin == p.unit_end:
                 p.unit_begin = p.unit_end = -1  # (0, 0 means "everything" in the ABI; an empty range must stay empty)
+        if out_dtype not in (torch.float32, torch.bfloat16):
+            raise ValidationError("out_dtype must be torch.float32 or torch.bfloat16")
+        p.out_bf16 = 1 if out_dtype == torch.bfloat16 else 0
         if out is not None:
-            if out.shape != (B, H, N, d) or out.dtype != torch.float32 or not out.is_contiguous():
-                raise ShapeError("attention: out must be a contiguous float32 [B,H,N,d] tensor")
+            if out.shape != (B, H, N, d) or out.dtype != out_dtype or not out.is_contiguous():
+                raise ShapeError(f"attention: out must be a contiguous {out_dtype} [B,H,N,d] tensor")
             O = out
         else:
-            O = (torch.zeros if units is not None else torch.empty)((B, H, N, d), dtype=torch.float32, device=Q.device)
+            O = (torch.zeros if units is not None else torch.empty)((B, H, N, d), dtype=out_dtype, device=Q.device)
         if units is not None and p.unit_begin < 0:
             return O
         m = torch.empty((B, H, N), dtype=torch.float32, device=Q.device) if return_stats else None
@@ -389,7 +395,7 @@ class BinaryAttention:
                                                 _ptr(m), _ptr(l), None, self._stream()))
         return (O, m, l) if return_stats else O
 
-    def forward_host(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None):
+    def forward_host(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None, out_dtype=torch.float32):
         """Same call with HOST tensors (ideally pinned): H2D + kernels + D2H inside ba_binary_attention_host."""
         if Q.is_cuda or K.is_cuda or V.is_cuda:
             raise ValidationError("forward_host takes CPU tensors")
@@ -401,8 +407,13 @@ class BinaryAttention:
         if bias_t is not None and not isinstance(bias, (Relative1dBias, Relative2dBias)):
             bias = bias_t = bias_t.contiguous()
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        if out_dtype not in (torch.float32, torch.bfloat16):
+            raise ValidationError("out_dtype must be torch.float32 or torch.bfloat16")
+        p.out_bf16 = 1 if out_dtype == torch.bfloat16 else 0
         if out is None:
-            out = torch.empty((B, H, N, d), dtype=torch.float32, pin_memory=True)
+            out = torch.empty((B, H, N, d), dtype=out_dtype, pin_memory=True)
+        elif out.shape != (B, H, N, d) or out.dtype != out_dtype or not out.is_contiguous():
+            raise ShapeError(f"attention: out must be a contiguous {out_dtype} [B,H,N,d] tensor")
         _check(self.lib.ba_binary_attention_host(self.h, C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(bias_t), _ptr(out),
                                                  None, None))
         return out

@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
         for (int c = 0; c < kI8Slice; ++c) o[c] = o[c] * rescale + (float)acc[c];
     }
     if (!row_ok) return;
-    float* orow = a.O + ((int64_t)head * N + row) * d + sl * kI8Slice;
+    const int64_t obase = ((int64_t)head * N + row) * d + sl * kI8Slice;
 #pragma unroll
     for (int c = 0; c < kI8Slice; ++c)
-        if (sl * kI8Slice + c < d) orow[c] = o[c] / l / 255.0f * (float)scales[(int64_t)head * d + sl * kI8Slice + c];
+        if (sl * kI8Slice + c < d) store_out(a, obase + c, o[c] / l / 255.0f * (float)scales[(int64_t)head * d + sl * kI8Slice + c]);
     if (sl == 0) {
         if (a.row_max) a.row_max[(int64_t)head * N + row] = m;
         if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l;

@@ -98,10 +98,10 @@ __global__ void __launch_bounds__(kSimtRows * 8, 1) attn_simt_kernel(const __gri
     }
     if (!row_ok) return;
     const float inv_l = 1.0f / l;
-    float* orow = a.O + ((int64_t)head * N + row) * d + sl * kSimtSlice;
+    const int64_t obase = ((int64_t)head * N + row) * d + sl * kSimtSlice;
 #pragma unroll
     for (int c = 0; c < kSimtSlice; ++c)
-        if (sl * kSimtSlice + c < d) orow[c] = o[c] * inv_l;
+        if (sl * kSimtSlice + c < d) store_out(a, obase + c, o[c] * inv_l);
     if (sl == 0) {
         if (a.row_max) a.row_max[(int64_t)head * N + row] = m * kLn2;  // back to natural units
         if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l;

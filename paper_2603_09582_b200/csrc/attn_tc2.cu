@@ -20,7 +20,7 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     if (!tc2_shape_ok(a.in_dtype, a.N, a.d) || !a.k_exp || !a.q_exp) return 0;
     if (dbg_S && a.N % TN != 0) return 0;  // (the logits dump has no ragged instantiation)
     if (a.d % 8 != 0 || a.d > 128) return 0;
-    if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % 32 != 0) return 0;
+    if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % (a.out_bf16 ? 16 : 32) != 0) return 0;
     int bias_mode = 0;
     int g = 0;
     if (a.bias && a.bias_kind == BA_BIAS_REL2D) {
@@ -82,12 +82,15 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
-    {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 16 floats (64 B, 64B swizzle), clipped at N and d by the hardware
+    {   // O: [BH, N, d] fp32 (or bf16, ba_params.out_bf16); per-warp boxes of 32 rows x 16 elements (64 B with the 64B swizzle,
+        // or 32 B with the 32B swizzle), clipped at N and d by the hardware
+        const cuuint64_t esz = a.out_bf16 ? 2 : 4;
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
-        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * esz, (cuuint64_t)a.N * a.d * esz};
         const cuuint32_t box[3] = {16, 32, 1};
-        if (enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        if (enc(&omap, a.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, a.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
     bmap = vmap;

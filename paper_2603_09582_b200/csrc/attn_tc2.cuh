@@ -558,6 +558,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             const float l = (l0 + l1) + sm->xch[X][half ^ 1][r];
             const float inv_l = 1.0f / l;
             float* orow = a.O + ((int64_t)head * N + row) * d;
+            __nv_bfloat16* orow16 = reinterpret_cast<__nv_bfloat16*>(a.O) + ((int64_t)head * N + row) * d;  // (out_bf16)
             for (int c = oc0; c < oc1; c += 16) {
                 float o[16];
                 BA_TMEM_LD16(o_addr + c, o, 0);
@@ -572,10 +573,18 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     // Direct stores (32 lanes x 32 B to 32 different rows per instruction) keep the LSU busy for ~2000 clk per
                     // unit; a [32 rows][16 floats] box in shared memory (64B swizzle: 16-byte chunk q of row r sits at
                     // q ^ ((r >> 1) & 3)) goes out as ONE asynchronous TMA store, clipped at N and d by the hardware.
+                    if (a.out_bf16) {  // [32 rows][16 bf16]: 32-byte rows, 32B swizzle (chunk q of row r sits at q ^ ((r >> 2) & 1))
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        *reinterpret_cast<float4*>(box + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
-                            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                        for (int q = 0; q < 2; ++q)
+                            *reinterpret_cast<uint4*>(box + lane * 32 + ((q ^ ((lane >> 2) & 1)) << 4)) =
+                                make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
+                                           pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            *reinterpret_cast<float4*>(box + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                                make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                    }
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
@@ -583,8 +592,17 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 } else if (row < N) {
-                    if (c + 8 <= d) stg_256(orow + c, o);
-                    if (c + 16 <= d) stg_256(orow + c + 8, o + 8);
+                    if (a.out_bf16) {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+                            if (c + 8 * q + 8 <= d)
+                                *reinterpret_cast<uint4*>(orow16 + c + 8 * q) =
+                                    make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
+                                               pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+                    } else {
+                        if (c + 8 <= d) stg_256(orow + c, o);
+                        if (c + 16 <= d) stg_256(orow + c + 8, o + 8);
+                    }
                 }
             }
             tc_fence_before();

@@ -127,12 +127,15 @@ int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
-    {   // O: fp32 [BH, N, d]; per-warp boxes of 32 rows x 32 floats (128 B), clipped at N and d by the hardware
+    {   // O: [BH, N, d] fp32 (or bf16, ba_params.out_bf16); per-warp boxes of 32 rows x 32 elements (128 B with the 128B
+        // swizzle, or 64 B with the 64B swizzle), clipped at N and d by the hardware
+        const cuuint64_t esz = a.out_bf16 ? 2 : 4;
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
-        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 4, (cuuint64_t)a.N * a.d * 4};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d * esz, (cuuint64_t)a.N * a.d * esz};
         const cuuint32_t box[3] = {32, 32, 1};
-        if (enc(&m.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        if (enc(&m.o, a.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.O, gdim, gstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, a.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
     m.b = m.v;

@@ -557,6 +557,7 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
         tc_fence_after();
         float l = ep.rs.l;
         float* orow = a.O + ((int64_t)ep.head * a.N + ep.row) * a.d;
+        __nv_bfloat16* orow16 = reinterpret_cast<__nv_bfloat16*>(a.O) + ((int64_t)ep.head * a.N + ep.row) * a.d;  // (out_bf16)
         for (int c = 0; c < prm.dvp; c += 32) {
             float o[32], den[16];
             const bool two = c + 16 < prm.dvp;
@@ -579,10 +580,18 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
                 }
+                if (a.out_bf16) {  // [32 rows][32 bf16]: 64-byte rows, 64B swizzle (chunk q of row r sits at q ^ ((r >> 1) & 3))
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<float4*>(box + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-                        make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                    for (int q = 0; q < 4; ++q)
+                        *reinterpret_cast<uint4*>(box + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
+                                       pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<float4*>(box + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                }
                 if (bi == 1 || c + 32 >= prm.dvp) {  // one proxy fence and one bulk group per pair of boxes
                     fence_proxy_async();
                     __syncwarp();
@@ -597,7 +606,11 @@ __device__ __forceinline__ void run_epilogue(Smem* sm, const Params& prm, const 
                 for (int q = 0; q < 4; ++q) {
                     const int cc = c + 8 * q;
                     if (cc + 8 <= a.d) {
-                        if (prm.o_vec8) {
+                        if (a.out_bf16) {  // 8 bf16 = 16 bytes (d % 8 == 0 and a 16-byte aligned O keep every chunk aligned)
+                            *reinterpret_cast<uint4*>(orow16 + cc) =
+                                make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
+                                           pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+                        } else if (prm.o_vec8) {
                             stg_256(orow + cc, o + 8 * q);
                         } else {
                             *reinterpret_cast<float4*>(orow + cc) = make_float4(o[8 * q], o[8 * q + 1], o[8 * q + 2], o[8 * q + 3]);

@@ -28,7 +28,8 @@ struct FwdArgs {
     const unsigned char* q_exp;  // [BH, ceil(N/256), 2, KPAD/16, 128, 16] the same for Q in 128-row tiles, two per unit
     const void* bias;         // dense: [bias_heads, N, bias_ld]; rel1d: [bias_heads, 2N-1]; or nullptr
     int bias_kind;            // BA_BIAS_NONE / BA_BIAS_DENSE / BA_BIAS_REL1D / BA_BIAS_REL2D ([bias_heads, 2, 2g-1]; tc2 kernel only)
-    float* O;                 // [BH, N, d] fp32
+    float* O;                 // [BH, N, d] fp32 -- or bf16 storage when out_bf16 (see store_out)
+    int out_bf16;             // ba_params.out_bf16
     float* row_max;           // [BH, N] or nullptr
     float* row_sum;           // [BH, N] or nullptr
     int64_t bias_ld;
@@ -84,6 +85,12 @@ __device__ __forceinline__ float load_as_float(const void* base, int dtype, int6
 }
 
 __host__ __device__ inline int dtype_size(int dtype) { return dtype == BA_F32 ? 4 : 2; }
+
+// One element of O (flat index over [BH, N, d]): float32, or bfloat16 rounded to nearest-even when the call asked for it.
+__device__ __forceinline__ void store_out(const FwdArgs& a, int64_t idx, float v) {
+    if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.O)[idx] = __float2bfloat16_rn(v);
+    else a.O[idx] = v;
+}
 
 // Shard units (BA_UNIT_ROWS = 256 query rows) of a call: count per head, and "does the call compute row `row` of head `head`".
 __host__ __device__ inline int units_per_head(int N) { return (N + 255) / 256; }

@@ -121,6 +121,7 @@ int check_params(const ba_params* p, bool need_attention) {
             return fail(BA_ERR_VALIDATION, "unit range [%lld, %lld) outside [0, %lld]", (long long)p->unit_begin,
                         (long long)p->unit_end, (long long)total);
     }
+    if (p->out_bf16 != 0 && p->out_bf16 != 1) return fail(BA_ERR_VALIDATION, "out_bf16 must be 0 (float32 O) or 1 (bfloat16 O)");
     if (p->quantize_pv) {
         const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
         if (bc < 1 || bc > p->N)  // attention.cpp:26-28
@@ -482,7 +483,7 @@ int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* 
 // One K1 + K2 pass over `heads` consecutive heads starting at grid index head0; every tensor pointer already points at
 // that first head.  `ws` holds make_layout(p, heads).total bytes, `tickets` 2*heads zeroed counters.
 static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0, int64_t heads, const void* Q, const void* K,
-                     const void* V, const void* bias, float* O, float* row_max, float* row_sum, char* ws,
+                     const void* V, const void* bias, void* O, float* row_max, float* row_sum, char* ws,
                      unsigned int* tickets, cudaStream_t stream, bool prof, int unit0 = 0, int unit1 = 0) {
     const Layout L = make_layout(p, heads);
     ba::FwdArgs a{};
@@ -501,7 +502,7 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
         const int g = grid_side(p->N);
         const bool in_kernel = kernel == BA_KERNEL_TCGEN05 && !p->quantize_pv && ba::tc2_shape_ok(p->in_dtype, p->N, p->d) &&
                                g % 32 == 0 && g <= 128 && !(getenv("BA_TC2") && atol(getenv("BA_TC2")) == 0) && a.k_exp &&
-                               reinterpret_cast<uintptr_t>(V) % 16 == 0 && reinterpret_cast<uintptr_t>(O) % 32 == 0;
+                               reinterpret_cast<uintptr_t>(V) % 16 == 0 && reinterpret_cast<uintptr_t>(O) % (p->out_bf16 ? 16 : 32) == 0;
         if (!in_kernel) {  // expand once into the handle's fp32 table and run the dense path (attention.cpp:78-96)
             const size_t need = (size_t)p->bias_heads * p->N * p->N * sizeof(float);
             int rc = ensure(&h->rel2d, &h->rel2d_bytes, need, false);
@@ -515,7 +516,8 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
             a.bias_ld = p->N;
         }
     }
-    a.O = O;
+    a.O = static_cast<float*>(O);
+    a.out_bf16 = p->out_bf16 ? 1 : 0;
     a.row_max = row_max;
     a.row_sum = row_sum;
     a.BH = (int)heads;
@@ -574,7 +576,7 @@ static int resolve_kernel(const ba_params* p, int* kernel) {
 }
 
 int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
-                            const void* bias, float* O, float* row_max, float* row_sum, void* workspace,
+                            const void* bias, void* O, float* row_max, float* row_sum, void* workspace,
                             void* stream_) {
     if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
     int rc = check_params(p, true);
@@ -600,9 +602,9 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
         // unit-sharded call: K1 (and K, V, the scales) for every head the range touches, the attention kernel for the range only
         const int upb = ba::units_per_head(p->N);
         const int64_t hb = p->unit_begin / upb, he = (p->unit_end - 1) / upb + 1;
-        const size_t in_head = (size_t)p->N * p->d * ba::dtype_size(p->in_dtype), out_head = (size_t)p->N * p->d * sizeof(float);
+        const size_t in_head = (size_t)p->N * p->d * ba::dtype_size(p->in_dtype), out_head = (size_t)p->N * p->d * (p->out_bf16 ? 2 : sizeof(float));
         return fwd_range(h, p, kernel, hb, he - hb, static_cast<const char*>(Q) + hb * in_head, static_cast<const char*>(K) + hb * in_head,
-                         static_cast<const char*>(V) + hb * in_head, bias, reinterpret_cast<float*>(reinterpret_cast<char*>(O) + hb * out_head),
+                         static_cast<const char*>(V) + hb * in_head, bias, static_cast<char*>(O) + hb * out_head,
                          row_max ? row_max + hb * p->N : nullptr, row_sum ? row_sum + hb * p->N : nullptr,
                          static_cast<char*>(workspace), h->tickets, stream, prof, (int)(p->unit_begin - hb * upb),
                          (int)(p->unit_end - hb * upb));
@@ -615,7 +617,7 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
 // Host-buffer call: the head grid is cut into chunks that flow through three streams -- H2D copies, K1+K2, D2H copies
 // -- so the two PCIe directions and the kernels overlap (the copies are asynchronous only for pinned host memory).
 int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, const void* K, const void* V,
-                             const void* bias, float* O, float* row_max, float* row_sum) {
+                             const void* bias, void* O, float* row_max, float* row_sum) {
     if (!h) return fail(BA_ERR_VALIDATION, "handle is NULL");
     int rc = check_params(p, true);
     if (rc) return rc;
@@ -627,7 +629,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     if ((rc = resolve_kernel(p, &kernel))) return rc;
     const size_t BH = (size_t)p->B * p->H;
     const size_t head_in = (size_t)p->N * p->d * ba::dtype_size(p->in_dtype);  // bytes of one head of Q, K or V
-    const size_t head_out = (size_t)p->N * p->d * sizeof(float);
+    const size_t head_out = (size_t)p->N * p->d * (p->out_bf16 ? 2 : sizeof(float));
     const size_t head_row = (size_t)p->N * sizeof(float);
     const size_t ld = p->bias_ld ? p->bias_ld : p->N;
     const size_t bias_bytes =
@@ -700,7 +702,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
         BA_CUDA(cudaEventRecord(h->ev_in[c], h->stream_in));
         BA_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
         rc = fwd_range(h, p, kernel, (int64_t)h0, (int64_t)nh, dQ + h0 * head_in, dK + h0 * head_in, dV + h0 * head_in,
-                       bias_bytes ? h->stage[3] : nullptr, reinterpret_cast<float*>(dO + h0 * head_out),
+                       bias_bytes ? h->stage[3] : nullptr, dO + h0 * head_out,
                        row_max ? reinterpret_cast<float*>(dM + h0 * head_row) : nullptr,
                        row_sum ? reinterpret_cast<float*>(dL + h0 * head_row) : nullptr,
                        static_cast<char*>(h->stage[7]) + (size_t)c * Lc.total, h->tickets + 2 * h0, h->stream, false);

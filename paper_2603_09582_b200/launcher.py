@@ -85,17 +85,20 @@ class ShardedBinaryAttention:
             bl = bias[idx[0]:idx[-1] + 1] if idx and contiguous else bias[idx]  # a view when the range does not wrap
         return cut(Q), cut(K), cut(V), bl
 
-    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto"):
+    def forward(self, Q, K, V, bias=None, scale=None, kernel="auto", out_dtype=None):
+        import torch
+        out_dtype = out_dtype or torch.float32
         if Q.shape[1] == 0:
-            import torch
-            return torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
-        return self.ba.forward(Q, K, V, bias, scale, kernel=kernel)
+            return torch.empty(Q.shape, dtype=out_dtype, device=Q.device)
+        return self.ba.forward(Q, K, V, bias, scale, kernel=kernel, out_dtype=out_dtype)
 
-    def forward_units(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None):
+    def forward_units(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None, out_dtype=None):
         """Unit-sharded forward on the FULL [B,H,N,d] tensors (resident on every rank): this rank computes its (head, 256-row
         block) units only; rows of other ranks' units stay zero in the returned tensor (sum or gather to combine)."""
         B, H, N = Q.shape[0], Q.shape[1], Q.shape[2]
-        return self.ba.forward(Q, K, V, bias, scale, kernel=kernel, units=shard_units(B, H, N, self.world, self.rank), out=out)
+        import torch
+        return self.ba.forward(Q, K, V, bias, scale, kernel=kernel, units=shard_units(B, H, N, self.world, self.rank), out=out,
+                               out_dtype=out_dtype or torch.float32)
 
     def gather(self, O_local, B: int, H: int):
         """All ranks' outputs as one [B,H,N,d] tensor (all_gather of equal-size padded shards; verification only)."""
