@@ -20,29 +20,114 @@ constexpr int kI8Slice = 32;    // O columns per thread
 constexpr int kI8MaxBc = 64;    // keys per block staged in shared memory
 constexpr int kI8MaxW64 = 4;    // d <= 256
 
-// One CTA per head: column abs-max (exact: max is order independent), then the s8 levels.
-__global__ void __launch_bounds__(kQvThreads) quantize_values_kernel(const void* V, int in_dtype, int N, int d, int8_t* vq,
-                                                                     double* scales) {
+// K1v, quantize_values (quantize.cpp:57-74) in three small launches over a (head, 256-row chunk) grid:
+//   A  column abs-max: per-thread running max over its rows, then one atomicMax per column and CTA on the LOW WORD of the
+//      head's scales[] slot (zeroed first; non-negative floats order like their bit patterns, and max is order independent,
+//      so the result is exact);
+//   B  levels: delta = amax / 127 (1 for an all-zero column) and round_half_away(v / delta), both in fp64 like the reference
+//      => bit-identical s8 levels;
+//   C  the slots become the fp64 scales.
+// Thread (ty, tx): tx = group of 8 consecutive columns, ty = row lane.  (The first build ran one CTA per head with a
+// shared-memory atomicMax per ELEMENT: ~0.4 ms at 16 heads x 4096 keys, more than the attention kernel it feeds.)
+constexpr int kQvChunk = 256;  // rows per CTA
+
+__device__ __forceinline__ void qv_load8(const void* V, int in_dtype, int64_t off, int c0, int d, float (&v)[8]) {
+    if (in_dtype != BA_F32 && c0 + 8 <= d && (off & 7) == 0) {  // 16 aligned bytes of bf16 / fp16
+        const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(V) + off);
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (in_dtype == BA_BF16) {
+                v[2 * i] = __uint_as_float(ww[i] << 16);
+                v[2 * i + 1] = __uint_as_float(ww[i] & 0xFFFF0000u);
+            } else {
+                const __half2 hh = *reinterpret_cast<const __half2*>(&ww[i]);
+                v[2 * i] = __low2float(hh);
+                v[2 * i + 1] = __high2float(hh);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = c0 + i < d ? load_as_float(V, in_dtype, off + i) : 0.f;
+    }
+}
+
+__global__ void __launch_bounds__(kQvThreads) qv_amax_kernel(const void* V, int in_dtype, int N, int d, int chunks, double* scales) {
     __shared__ unsigned int amax_bits[256];
-    __shared__ double delta[256];
-    const int head = blockIdx.x;
-    const int64_t base = (int64_t)head * N * d;
-    for (int c = threadIdx.x; c < d; c += kQvThreads) amax_bits[c] = 0u;
+    const int head = blockIdx.x / chunks, chunk = blockIdx.x - head * chunks;
+    const int cg = (d + 7) / 8, tx = threadIdx.x % cg, ty = threadIdx.x / cg, rows_per_pass = kQvThreads / cg;
+    for (int c = threadIdx.x; c < 256; c += kQvThreads) amax_bits[c] = 0u;
     __syncthreads();
-    for (int idx = threadIdx.x; idx < N * d; idx += kQvThreads) {
-        const float v = fabsf(load_as_float(V, in_dtype, base + idx));  // non-negative floats order like their bit patterns
-        atomicMax(&amax_bits[idx % d], __float_as_uint(v));
+    const int r1 = min(N, (chunk + 1) * kQvChunk);
+    if (ty < rows_per_pass) {
+        float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int row = chunk * kQvChunk + ty; row < r1; row += rows_per_pass) {
+            float v[8];
+            qv_load8(V, in_dtype, ((int64_t)head * N + row) * d + tx * 8, tx * 8, d, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], fabsf(v[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (tx * 8 + i < d) atomicMax(&amax_bits[tx * 8 + i], __float_as_uint(m[i]));
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < d; c += kQvThreads) {
-        const double amax = (double)__uint_as_float(amax_bits[c]);
-        const double s = amax > 0.0 ? amax / 127.0 : 1.0;  // quantize.cpp:61-66
-        delta[c] = s;
-        scales[(int64_t)head * d + c] = s;
+    unsigned int* slots = reinterpret_cast<unsigned int*>(scales + (int64_t)head * d);  // low word of each fp64 slot (little endian)
+    for (int c = threadIdx.x; c < d; c += kQvThreads) atomicMax(slots + 2 * c, amax_bits[c]);
+}
+
+__global__ void __launch_bounds__(kQvThreads) qv_levels_kernel(const void* V, int in_dtype, int N, int d, int chunks, const double* scales,
+                                                               int8_t* vq) {
+    const int head = blockIdx.x / chunks, chunk = blockIdx.x - head * chunks;
+    const int cg = (d + 7) / 8, tx = threadIdx.x % cg, ty = threadIdx.x / cg, rows_per_pass = kQvThreads / cg;
+    __shared__ double sdelta[256];
+    __shared__ float srdelta[256];
+    const unsigned int* slots = reinterpret_cast<const unsigned int*>(scales + (int64_t)head * d);
+    for (int c = threadIdx.x; c < 256; c += kQvThreads) {  // one pair of fp64 divisions per column and CTA, not per thread
+        const double amax = c < d ? (double)__uint_as_float(slots[2 * c]) : 0.0;
+        const double dl = amax > 0.0 ? amax / 127.0 : 1.0;  // quantize.cpp:61-66
+        sdelta[c] = dl;
+        srdelta[c] = (float)(1.0 / dl);
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < N * d; idx += kQvThreads)
-        vq[base + idx] = (int8_t)round((double)load_as_float(V, in_dtype, base + idx) / delta[idx % d]);  // round_half_away
+    if (ty >= rows_per_pass) return;
+    double delta[8];
+    float rdelta[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        delta[i] = sdelta[(tx * 8 + i) & 255];
+        rdelta[i] = srdelta[(tx * 8 + i) & 255];
+    }
+    const int r1 = min(N, (chunk + 1) * kQvChunk);
+    for (int row = chunk * kQvChunk + ty; row < r1; row += rows_per_pass) {
+        float v[8];
+        const int64_t off = ((int64_t)head * N + row) * d + tx * 8;
+        qv_load8(V, in_dtype, off, tx * 8, d, v);
+        int8_t q[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            // round_half_away(v / delta) in fp64 decides (quantize.cpp:68-72).  An fp32 estimate of the quotient is within
+            // 2e-5 of it (|v / delta| <= 127), so away from the rounding boundaries -- more than 1e-4 from a half-integer --
+            // both round to the same level and the fp64 division is skipped (it is ~20 instructions on a narrow pipe).
+            const float xe = v[i] * rdelta[i];
+            const float fr = fabsf(xe) - floorf(fabsf(xe));
+            q[i] = fabsf(fr - 0.5f) > 1e-4f ? (int8_t)__float2int_rn(xe) : (int8_t)round((double)v[i] / delta[i]);
+        }
+        if (tx * 8 + 8 <= d && (off & 7) == 0) {
+            *reinterpret_cast<uint2*>(vq + off) = *reinterpret_cast<const uint2*>(q);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (tx * 8 + i < d) vq[off + i] = q[i];
+        }
+    }
+}
+
+__global__ void qv_scales_kernel(double* scales, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double amax = (double)__uint_as_float(reinterpret_cast<const unsigned int*>(scales + i)[0]);
+    scales[i] = amax > 0.0 ? amax / 127.0 : 1.0;
 }
 
 __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_constant__ FwdArgs a, const int8_t* __restrict__ vq,
@@ -141,9 +226,15 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
 int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, double* scales,
                            cudaStream_t stream) {
     if (d > 256) return -(int)cudaErrorInvalidValue;
-    quantize_values_kernel<<<(unsigned)heads, kQvThreads, 0, stream>>>(V, in_dtype, N, d, vq, scales);
-    const cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 1 : -(int)e;
+    if (heads == 0 || N == 0) return 0;
+    const int chunks = (N + kQvChunk - 1) / kQvChunk;
+    cudaError_t e = cudaMemsetAsync(scales, 0, (size_t)heads * d * sizeof(double), stream);
+    if (e != cudaSuccess) return -(int)e;
+    qv_amax_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales);
+    qv_levels_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales, vq);
+    qv_scales_kernel<<<(unsigned)((heads * d + 255) / 256), 256, 0, stream>>>(scales, heads * d);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 3 : -(int)e;
 }
 
 int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream) {

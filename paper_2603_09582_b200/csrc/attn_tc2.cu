@@ -12,18 +12,38 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 EncodeTiledFn get_encode_fn();  // attn_tcgen05.cu
 }  // namespace tc
 
+static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vscales, int32_t* dbg_S, int dbg_head, long long* dbg_T,
+                          cudaStream_t stream);
+
 // Returns the number of kernels launched (> 0), a negative cudaError_t, or 0 when this kernel does not take the shape
 // (the caller then runs the first-generation kernel).
 int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* dbg_T, cudaStream_t stream) {
+    return launch_tc2_any(a, nullptr, nullptr, dbg_S, dbg_head, dbg_T, stream);
+}
+
+// quantize_pv = true on the tensor cores (the I8 mode of attn_tc2_kernel): vq = s8 value levels [BH, N, d], vscales = their
+// per-channel fp64 scales [BH, d] (K1v).  Takes block_cols = 64 (one key tile per block, the reference's default for N >= 64),
+// bf16-packed inputs with d % 16 == 0, d <= 64, N >= 128 and no bias or a TMA-able dense bf16 table; 0 otherwise (the caller
+// then runs the CUDA-core kernel).
+int launch_attn_tc2_i8(const FwdArgs& a, const int8_t* vq, const double* vscales, int block_cols, cudaStream_t stream) {
+    if (tc::env_long("BA_TC2_I8", 1) == 0 || block_cols != 64 || !vq || !vscales) return 0;
+    if (!tc2_i8_shape_ok(a.in_dtype, a.N, a.d) || reinterpret_cast<uintptr_t>(vq) % 16 != 0) return 0;
+    return launch_tc2_any(a, vq, vscales, nullptr, 0, nullptr, stream);
+}
+
+static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vscales, int32_t* dbg_S, int dbg_head, long long* dbg_T,
+                          cudaStream_t stream) {
     using namespace tc2;
-    if (env_long("BA_TC2", 1) == 0) return 0;
-    if (!tc2_shape_ok(a.in_dtype, a.N, a.d) || !a.k_exp || !a.q_exp) return 0;
+    const bool i8 = vq != nullptr;
+    if (env_long("BA_TC2", 1) == 0 && !i8) return 0;
+    if (!(i8 || tc2_shape_ok(a.in_dtype, a.N, a.d)) || !a.k_exp || !a.q_exp) return 0;
     if (dbg_S && a.N % TN != 0) return 0;  // (the logits dump has no ragged instantiation)
     if (a.d % 8 != 0 || a.d > 128) return 0;
-    if (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % (a.out_bf16 ? 16 : 32) != 0) return 0;
+    if (!i8 && (reinterpret_cast<uintptr_t>(a.V) % 16 != 0 || reinterpret_cast<uintptr_t>(a.O) % (a.out_bf16 ? 16 : 32) != 0)) return 0;
     int bias_mode = 0;
     int g = 0;
     if (a.bias && a.bias_kind == BA_BIAS_REL2D) {
+        if (i8) return 0;
         g = (int)std::lround(std::sqrt((double)a.N));
         if ((long long)g * g != a.N || g % 32 != 0 || g > 128) return 0;  // (the C-ABI layer expands the table for these)
         bias_mode = 4;
@@ -31,7 +51,7 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
         if (a.bias_kind != BA_BIAS_DENSE) return 0;
         const bool tma_ok = a.bias_dtype == BA_BF16 && (a.bias_ld * 2) % 16 == 0 && reinterpret_cast<uintptr_t>(a.bias) % 16 == 0;
         if (!tma_ok) return 0;
-        if (a.N < env_long("BA_TC2_MIN_N_BIAS", 2048)) return 0;  // with a dense bias the first-generation kernel is level or ahead below ~2048 keys (measured)
+        if (!i8 && a.N < env_long("BA_TC2_MIN_N_BIAS", 2048)) return 0;  // with a dense bias the first-generation kernel is level or ahead below ~2048 keys (measured)
         bias_mode = 1;
     }
     tc::EncodeTiledFn enc = tc::get_encode_fn();
@@ -53,6 +73,8 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
     prm.dbg_head = dbg_head;
     prm.g = g;
     prm.dbg_T = dbg_T;
+    prm.vbox = i8 ? kVBox8 : kVBox;
+    prm.vscales = vscales;
     const int kpad = (a.d + 31) / 32 * 32;
     // ring depths: as deep as 227 KB allow; the bias ring must cover the HBM latency of the N x N stream
     prm.kst = 4;
@@ -73,7 +95,14 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
 
     CUtensorMap vmap, bmap, omap;
     const cuuint32_t estr[3] = {1, 1, 1};
-    {
+    if (i8) {  // s8 value levels [BH, N, d]: boxes of 64 keys x 64 channels (64 B rows, 64B swizzle; channels past d read as 0)
+        const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
+        const cuuint64_t gstr[2] = {(cuuint64_t)a.d, (cuuint64_t)a.N * a.d};
+        const cuuint32_t box[3] = {64, (cuuint32_t)TN, 1};
+        if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(vq), gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -(int)cudaErrorInvalidValue;
+    } else {
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
         const cuuint64_t gstr[2] = {(cuuint64_t)a.d * 2, (cuuint64_t)a.N * a.d * 2};
         const cuuint32_t box[3] = {64, (cuuint32_t)TN, 1};
@@ -106,6 +135,7 @@ int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* d
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
+    if (i8) return kpad == 32 ? launch_i8<32>(prm, bias_mode, vmap, bmap, omap, stream) : launch_i8<64>(prm, bias_mode, vmap, bmap, omap, stream);
     switch (kpad) {
         case 32: return launch_kpad2<32>(prm, bias_mode, vmap, bmap, omap, stream);
         case 64: return launch_kpad2<64>(prm, bias_mode, vmap, bmap, omap, stream);

@@ -42,6 +42,7 @@ constexpr int TN = 64;             // keys per tile (UMMA N of the S MMA)
 constexpr int kThreads2 = 640;
 constexpr int kColO2 = 256;        // first O column; tile X owns [256 + 128 X, +dvp)
 constexpr int kVBox = 8192;        // one TMA box of V: 64 keys x 64 columns bf16, 128B swizzle
+constexpr int kVBox8 = 4096;       // I8: one TMA box of the s8 value levels: 64 keys x 64 columns, 64B swizzle
 constexpr int kOStage = 16 * 2048;  // epilogue staging: 16 warps x one 2 KB box ([32 rows][16 floats], 64B swizzle)
 constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16, 128B swizzle
 #ifndef BA_PP_AT
@@ -66,6 +67,7 @@ struct Smem2 {
     float xch[2][2][TM];          // (query tile, column half, row): half-row max / partial denominator for the other half
     uint32_t flag[2][2][4][2];    // (tile parity, query tile, lane quadrant, column half): "my warp needs a new reference max"
     float rel2[3][2][256];        // BIAS 4: row / col offset tables (2g-1 <= 255 entries) of the heads of three consecutive units
+    float xch8[2][2][2][TM];      // I8: (tile parity, query tile, column half, row) block max of my half, every tile
     uint32_t tmem_base;
 };
 
@@ -80,6 +82,8 @@ struct Params2 {
     int qst, kst, vst, bst;
     int o_stage;   // the epilogue goes through per-warp staging boxes and TMA stores (when 32 KB of shared memory are left)
     int g;         // BIAS 4: grid side sqrt(N) (a multiple of 32)
+    int vbox;      // bytes of one V box in shared memory (kVBox, or kVBox8 in the I8 mode)
+    const double* vscales;  // I8: [BH, d] per-channel value scales (quantize_values, quantize.cpp:57-74)
     int32_t* dbg_S;
     int dbg_head;
     long long* dbg_T;
@@ -98,6 +102,23 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                  : "memory");
 }
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+// D[tmem] (s32) (+)= A[tmem] (u8, K-major: lane = row, one 32-bit column = four K elements) * B[smem] (s8)
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// s32 accumulator word (arrived through a float register) -> float, exactly, for |v| < 2^22 (a tile's P.V is at most
+// 64 * 255 * 127 < 2^21): integer add into the mantissa of 1.5 * 2^23, then subtract it -- ALU + FMA pipe instead of I2F.
+__device__ __forceinline__ float s32_to_float(float bits) {
+    return __int_as_float(__float_as_int(bits) + 0x4B400000) - 12582912.0f;
+}
+#define BA_TMEM_ST8U(taddr, v)                                                                                  \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0,%1,%2,%3,%4,%5,%6,%7};"                        \
+                 ::"r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(taddr) \
+                 : "memory")
 // Per-thread constants of the softmax loop (addresses derived from %tid) are passed through this so that they live in a
 // register: left alone, the compiler re-derives them from %tid in every key tile (a dozen S2R + ~40 integer instructions
 // per tile in a loop whose issue slots are the bound).
@@ -131,14 +152,20 @@ __device__ __forceinline__ void sts_u32_volatile(uint32_t addr, uint32_t v) {
         if (TL && tl_buf && tl_n < kTlStamps) tl_buf[tl_n++] = clock64(); \
     } while (0)
 
-template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
+// I8: the reference's integer P.V mode (quantize_pv = true, attention.cpp:332-343, 361-363) with block_cols = 64 = one key tile:
+// per tile the TRUE running max (no lazy rescale: the u8 weight grid is relative to the running max after each block),
+// P8 = round(255 * exp(S - m_new)) as u8 A operand in TMEM, s8 value levels (K1v) as MN-major B operand, tcgen05.mma.kind::i8 into
+// a FRESH s32 accumulator per tile; the softmax threads fold it into an fp32 O kept in TMEM one tile later:
+// O = O * rescale + acc.  TMEM per query tile X (256 columns): S stages [0,128), s32 accumulator [128,192), fp32 O [192,256)
+// => d <= 64.  Epilogue: O / l / 255 * delta[c].
+template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false, bool I8 = false>
 __global__ void __launch_bounds__(kThreads2, 1)
 attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUtensorMap vmap,
                 const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap omap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const FwdArgs& a = prm.a;
     unsigned char* sV = smem_raw;                               // vst x nbox x 8 KB
-    unsigned char* sB = sV + prm.vst * prm.nbox * kVBox;        // bst x 16 KB
+    unsigned char* sB = sV + prm.vst * prm.nbox * prm.vbox;     // bst x 16 KB
     unsigned char* sQ = sB + prm.bst * kBSub;                   // qst x 256 x KPAD (tile A rows, then tile B rows)
     unsigned char* sO = sQ + prm.qst * 2 * TM * KPAD;           // o_stage x 16 x 2 KB: one [32 rows][16 floats] staging box per softmax warp
     unsigned char* sK = sO + prm.o_stage * kOStage;             // kst x 64 x KPAD
@@ -204,12 +231,13 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             // asynchronously) and only falls back to a blocking wait for the ones still open.
             const int X = warp - 16;
             const uint32_t idesc_s = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-            const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(prm.dvp >> 3) << 17) |
-                                      ((uint32_t)(TM >> 4) << 24);
+            // P.V: fp32 += bf16 x bf16 (B MN-major), or (I8) s32 = u8 x s8 (B MN-major)
+            const uint32_t idesc_pv = (I8 ? (2u << 4) | (0u << 7) | (1u << 10) : (1u << 4) | (1u << 7) | (1u << 10)) | (1u << 16) |
+                                      ((uint32_t)(prm.dvp >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
             const uint64_t q_desc = make_desc(smem_u32(sQ) + X * TM * KPAD, TM * 16, 128, 0);
             const uint64_t k_desc = make_desc(smem_u32(sK), TN * 16, 128, 0);
-            const uint64_t v_desc = make_desc(smem_u32(sV), kVBox, 1024, 2);
-            const uint32_t s_tmem = tmem + X * 128, o_tmem = tmem + kColO2 + X * 128;
+            const uint64_t v_desc = I8 ? make_desc(smem_u32(sV), kVBox8, 512, 4) : make_desc(smem_u32(sV), kVBox, 1024, 2);
+            const uint32_t s_tmem = tmem + (I8 ? X * 256 : X * 128), o_tmem = I8 ? s_tmem + 128 : tmem + kColO2 + X * 128;
             // Issue order per key tile j: S(j), then P.V(j-1) once P(j-1) has arrived.  S(j) overwrites the stage that held
             // P(j-2), read by P.V(j-2) an iteration earlier (tcgen05.mma executes in issue order), and must not wait for P(j-1).
             // The barriers of an iteration are polled up front with test_wait (non-blocking; try_wait may sleep on an open
@@ -265,13 +293,19 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                             if (pj == 0 && up > 0) mbar_wait(&sm->ofree[X], (up - 1) & 1u);  // the epilogue has read the old O
                             BA_STAMP2();
                             tc_fence_after();
-                            const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * kVBox) >> 4);
+                            const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * prm.vbox) >> 4);
                             const uint32_t p_tmem = s_tmem + pst * TN;
                             if (elect_one()) {
+                                if (I8) {  // two K = 32 steps; a fresh accumulator every tile; P8 of half h sits at column 32 h
 #pragma unroll
-                                for (int ks = 0; ks < TN / 16; ++ks)
-                                    mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
-                                                (pj > 0 || ks > 0) ? 1u : 0u);
+                                    for (int ks = 0; ks < TN / 32; ++ks)
+                                        mma_i8_ts(o_tmem, p_tmem + ks * 32, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv, ks > 0 ? 1u : 0u);
+                                } else {
+#pragma unroll
+                                    for (int ks = 0; ks < TN / 16; ++ks)
+                                        mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
+                                                    (pj > 0 || ks > 0) ? 1u : 0u);
+                                }
                                 tc_commit(&sm->pvdone[X][pst]);
                                 tc_commit(&sm->vfree[pvs]);
                             }
@@ -300,13 +334,19 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     mbar_wait(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
                     if (pj == 0 && up > 0) mbar_wait(&sm->ofree[X], (up - 1) & 1u);
                     tc_fence_after();
-                    const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * kVBox) >> 4);
+                    const uint64_t vd = v_desc + (uint64_t)((pvs * prm.nbox * prm.vbox) >> 4);
                     const uint32_t p_tmem = s_tmem + pst * TN;
                     if (elect_one()) {
+                        if (I8) {
 #pragma unroll
-                        for (int ks = 0; ks < TN / 16; ++ks)
-                            mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
-                                        (pj > 0 || ks > 0) ? 1u : 0u);
+                            for (int ks = 0; ks < TN / 32; ++ks)
+                                mma_i8_ts(o_tmem, p_tmem + ks * 32, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv, ks > 0 ? 1u : 0u);
+                        } else {
+#pragma unroll
+                            for (int ks = 0; ks < TN / 16; ++ks)
+                                mma_bf16_ts(o_tmem, p_tmem + (ks >> 1) * 32 + (ks & 1) * 8, vd + (uint64_t)(ks * (2048 >> 4)), idesc_pv,
+                                            (pj > 0 || ks > 0) ? 1u : 0u);
+                        }
                         tc_commit(&sm->pvdone[X][pst]);
                         tc_commit(&sm->vfree[pvs]);
                     }
@@ -344,9 +384,9 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         bulk_load(sK + kr.stage * TN * KPAD, a.k_exp + ((int64_t)head * T + j) * (TN * KPAD), TN * KPAD, &sm->kfull[kr.stage]);
                         kr.next(prm.kst);
                         mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
-                        mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * kVBox);
+                        mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * prm.vbox);
                         for (int b = 0; b < prm.nbox; ++b)
-                            tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * kVBox, b * 64, j * TN, head);
+                            tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * prm.vbox, b * 64, j * TN, head);
                         vr.next(prm.vst);
                     }
                 }
@@ -379,13 +419,13 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
         const int X = warp >> 3, half = (warp >> 2) & 1, quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-        const uint32_t s_base = keep_u32(lane_base + X * 128 + half * 32);  // + 64 * stage: my 32 S columns; P goes over the first 16
+        const uint32_t s_base = keep_u32(lane_base + (I8 ? X * 256 : X * 128) + half * 32);  // + 64 * stage: my 32 S columns; P goes over the first 16 (I8: 8)
         // my row of a bias tile: 16-byte chunk (half*4 + c) ^ (r & 7) of row r = (this address) ^ (c << 4) (+ the stage offset;
         // the ring is 1024-byte aligned)
         const uint32_t b_thr = keep_u32(smem_u32(sB) + r * 128 + ((((uint32_t)half << 2) ^ (uint32_t)(r & 7)) << 4));
         const uint32_t fl_thr = keep_u32(smem_u32(&sm->flag[0][X][quad][0]));  // + (gx & 1) * sizeof(flag[0]); [half] = mine
         const uint32_t lane0 = keep_u32(lane == 0 ? 1u : 0u);
-        const uint32_t o_addr = lane_base + kColO2 + X * 128;
+        const uint32_t o_addr = I8 ? lane_base + X * 256 + 128 : lane_base + kColO2 + X * 128;  // O (I8: the s32 accumulator; fp32 O at + 64)
         const int pair_id = 1 + X * 4 + quad;
         const int h16 = ((prm.dvp >> 1) + 15) & ~15;             // O columns [0,h16) belong to half 0, [h16,dvp) to half 1
         const int oc0 = half ? h16 : 0, oc1 = half ? prm.dvp : h16;
@@ -421,7 +461,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 muk_n = __ldg(a.mu_k + (u + G) / prm.ublocks);
             }
             const float ea = (BIAS == 0) ? sc * kLog2e : kLog2e;  // BIAS 0 keeps x = raw dot and folds the scale into the exponent
-            const bool fast = BIAS == 0 && !stats && !DBG && sc * kLog2e * (float)d <= kFastBound;
+            const bool fast = BIAS == 0 && !I8 && !stats && !DBG && sc * kLog2e * (float)d <= kFastBound;
             float m_ref = fast ? sc * kLog2e * (float)d : -INFINITY, m_true = -INFINITY;
             float l0 = 0.f, l1 = 0.f;
             const bool dump = DBG && prm.dbg_S && head == prm.dbg_head;
@@ -430,6 +470,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             const float* rowtab = &sm->rel2[usm % 3][0][0];
             const float* coltab = &sm->rel2[usm % 3][1][0];
             float x[32];
+            float m_run = -INFINITY, rs_prev = 0.f;  // I8: running max (log2 units); rescale of the tile whose P.V is still to be folded into O
             for (int j = 0; j < T; ++j, ++gx) {
                 const uint32_t st = gx & 1u, par = (gx >> 1) & 1u;
                 const uint32_t s_addr = s_base + st * TN;
@@ -482,6 +523,64 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         if (i >= nk) x[i] = -INFINITY;
+                }
+                if (I8) {
+                    // ---- block max, agreed between the two halves EVERY tile (attention.cpp:306-310)
+                    float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
+#pragma unroll
+                    for (int i = 4; i < 32; i += 4) {
+                        m0 = fmaxf(m0, x[i]);
+                        m1 = fmaxf(m1, x[i + 1]);
+                        m2 = fmaxf(m2, x[i + 2]);
+                        m3 = fmaxf(m3, x[i + 3]);
+                    }
+                    const float hm = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * ea;
+                    sm->xch8[gx & 1u][X][half][r] = hm;
+                    pair_sync(pair_id);
+                    const float m_new = fmaxf(m_run, fmaxf(hm, sm->xch8[gx & 1u][X][half ^ 1][r]));
+                    const float rs = ex2(m_run - m_new);  // first block: 2^-inf = 0
+                    // ---- fold the previous tile's integer P.V into the fp32 O: O = O * rescale(prev) + acc(prev)
+                    if (j > 0) {
+                        mbar_wait(&sm->pvdone[X][st ^ 1u], ((gx - 1) >> 1) & 1u);
+                        tc_fence_after();
+                        for (int c = oc0; c < oc1; c += 16) {
+                            float acc[16], of[16];
+                            BA_TMEM_LD16(o_addr + c, acc, 0);
+                            if (j > 1) BA_TMEM_LD16(o_addr + 64 + c, of, 0);
+                            tc_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                of[i] = j > 1 ? fmaf(of[i], rs_prev, s32_to_float(acc[i])) : s32_to_float(acc[i]);
+                            BA_TMEM_ST16(o_addr + 64 + c, of, 0);
+                        }
+                    }
+                    rs_prev = rs;
+                    m_run = m_new;
+                    // ---- weights: P = 2^(x - m_new), l = l * rescale + sum P, P8 = round_half_away(255 P) (attention.cpp:312-337)
+                    l0 *= rs;
+                    l1 *= rs;
+                    // round(255 P) without the conversion unit (it shares the 16-per-clock pipe with ex2): 255 P + 1.5 * 2^23 rounds
+                    // to the nearest integer in the low mantissa bits.  Nearest-even there equals the reference's half-away
+                    // rounding for every float P: a tie needs 255 P = k + 1/2, i.e. P = (2k+1)/510, which no binary float is.
+                    uint32_t pk8[8];
+                    const float nm8 = -m_new;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        float a0, a1, a2, a3;
+                        fma2(a0, a1, x[4 * e], x[4 * e + 1], ea, ea, nm8, nm8);
+                        fma2(a2, a3, x[4 * e + 2], x[4 * e + 3], ea, ea, nm8, nm8);
+                        const float p0 = ex2(a0), p1 = ex2(a1), p2 = ex2(a2), p3 = ex2(a3);
+                        add2(l0, l1, p0, p1);
+                        add2(l0, l1, p2, p3);
+                        const uint32_t t0 = __float_as_uint(fmaf(p0, 255.0f, 12582912.0f)), t1 = __float_as_uint(fmaf(p1, 255.0f, 12582912.0f));
+                        const uint32_t t2 = __float_as_uint(fmaf(p2, 255.0f, 12582912.0f)), t3 = __float_as_uint(fmaf(p3, 255.0f, 12582912.0f));
+                        pk8[e] = __byte_perm(__byte_perm(t0, t1, 0x0040), __byte_perm(t2, t3, 0x0040), 0x5410);  // low bytes of t0..t3
+                    }
+                    BA_TMEM_ST8U(s_addr, pk8);
+                    tc_wait_st();
+                    tc_fence_before();
+                    warp_arrive(&sm->pfull[X][st], (int)(lane0 ^ 1u));
+                    continue;
                 }
                 if (!fast) {
                     float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
@@ -556,19 +655,29 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             sm->xch[X][half][r] = l0 + l1;
             pair_sync(pair_id);
             const float l = (l0 + l1) + sm->xch[X][half ^ 1][r];
-            const float inv_l = 1.0f / l;
+            const float inv_l = I8 ? 1.0f / l / 255.0f : 1.0f / l;
             float* orow = a.O + ((int64_t)head * N + row) * d;
             __nv_bfloat16* orow16 = reinterpret_cast<__nv_bfloat16*>(a.O) + ((int64_t)head * N + row) * d;  // (out_bf16)
             for (int c = oc0; c < oc1; c += 16) {
-                float o[16];
+                float o[16], of[16];
                 BA_TMEM_LD16(o_addr + c, o, 0);
+                if (I8 && T > 1) BA_TMEM_LD16(o_addr + 64 + c, of, 0);
                 if (prm.o_stage) {  // the box is free again once the TMA unit has READ the previous chunk out of it
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
                 }
                 tc_wait_ld();
+                if (I8) {  // O = (O * rescale(last) + acc(last)) / l / 255 * delta[c]  (attention.cpp:338-343, 361-363); d % 16 == 0
+                    const double* dl = prm.vscales + (int64_t)head * d + c;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) o[i] *= inv_l;
+                    for (int i = 0; i < 16; ++i) {
+                        const float acc = s32_to_float(o[i]);
+                        o[i] = (T > 1 ? fmaf(of[i], rs_prev, acc) : acc) * inv_l * (float)__ldg(dl + i);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[i] *= inv_l;
+                }
                 if (prm.o_stage) {
                     // Direct stores (32 lanes x 32 B to 32 different rows per instruction) keep the LSU busy for ~2000 clk per
                     // unit; a [32 rows][16 floats] box in shared memory (64B swizzle: 16-byte chunk q of row r sits at
@@ -607,8 +716,8 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             }
             tc_fence_before();
             if (stats && half == 0 && row < N) {
-                if (a.row_max) a.row_max[(int64_t)head * N + row] = m_true * kLn2;
-                if (a.row_sum) a.row_sum[(int64_t)head * N + row] = l * ex2(m_ref - m_true);
+                if (a.row_max) a.row_max[(int64_t)head * N + row] = (I8 ? m_run : m_true) * kLn2;
+                if (a.row_sum) a.row_sum[(int64_t)head * N + row] = I8 ? l : l * ex2(m_ref - m_true);
             }
             warp_arrive(&sm->ofree[X], lane);
         }
@@ -673,16 +782,16 @@ static int launch_expand_qk(const FwdArgs& a, int ktiles, int ublocks, cudaStrea
 constexpr size_t kSmemMax2 = 227 * 1024;
 
 inline size_t smem_bytes2(const Params2& p, int kpad) {
-    return (size_t)p.vst * p.nbox * kVBox + (size_t)p.bst * kBSub + (size_t)p.qst * 2 * TM * kpad + (size_t)p.kst * TN * kpad +
+    return (size_t)p.vst * p.nbox * p.vbox + (size_t)p.bst * kBSub + (size_t)p.qst * 2 * TM * kpad + (size_t)p.kst * TN * kpad +
            (size_t)p.o_stage * kOStage + sizeof(Smem2);
 }
 
-template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false>
+template <int KPAD, int BIAS, bool DBG, bool TL = false, bool RAGGED = false, bool I8 = false>
 static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
     static bool configured[kMaxDevices] = {};
     const int dev = current_device();
     if (!configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)kSmemMax2);
         if (e != cudaSuccess) return -(int)e;
         configured[dev] = true;
@@ -699,7 +808,7 @@ static int launch_variant2(const Params2& prm, const CUtensorMap& vmap, const CU
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = env_long("BA_PDL", 1) ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED>, prm, vmap, bmap, omap);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc2_kernel<KPAD, BIAS, DBG, TL, RAGGED, I8>, prm, vmap, bmap, omap);
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
@@ -731,6 +840,21 @@ static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vm
     }
     if (bias_mode == 1) return launch_variant2<KPAD, 1, false>(prm, vmap, bmap, omap, stream);
     return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, omap, stream);
+}
+
+// I8 mode (quantize_pv = true on the tensor cores): d <= 64, so KPAD is 32 or 64; bias none or the dense bf16 TMA table.
+template <int KPAD>
+static int launch_i8(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
+    const int ne = launch_expand_qk<KPAD>(prm.a, prm.tiles, prm.ublocks, stream);
+    if (ne < 0) return ne;
+    int nk;
+    if (prm.a.N % TN != 0)
+        nk = bias_mode == 1 ? launch_variant2<KPAD, 1, false, false, true, true>(prm, vmap, bmap, omap, stream)
+                            : launch_variant2<KPAD, 0, false, false, true, true>(prm, vmap, bmap, omap, stream);
+    else
+        nk = bias_mode == 1 ? launch_variant2<KPAD, 1, false, false, false, true>(prm, vmap, bmap, omap, stream)
+                            : launch_variant2<KPAD, 0, false, false, false, true>(prm, vmap, bmap, omap, stream);
+    return nk < 0 ? nk : ne + nk;
 }
 
 }  // namespace tc2

@@ -71,7 +71,8 @@ Layout make_layout(const ba_params* p, int64_t heads = -1) {
     }
     L.kexp = off;  // expanded K plane of the second-generation tcgen05 kernel (e4m3 +-1.0 bytes, UMMA tile order)
     L.qexp = off;
-    if (!p->quantize_pv && p->kernel != BA_KERNEL_SIMT && ba::tc2_shape_ok(p->in_dtype, p->N, p->d)) {
+    if (p->kernel != BA_KERNEL_SIMT &&
+        (p->quantize_pv ? ba::tc2_i8_shape_ok(p->in_dtype, p->N, p->d) : ba::tc2_shape_ok(p->in_dtype, p->N, p->d))) {
         off += align_up(ba::tc2_kexp_bytes(L.BH, p->N, p->d), 256);
         L.qexp = off;
         off += align_up(ba::tc2_qexp_bytes(L.BH, p->N, p->d), 256);
@@ -546,7 +547,14 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
         n = ba::launch_quantize_values(V, p->in_dtype, heads, p->N, p->d, vq, vs, stream);
         if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
         h->launches += n;
-        n = ba::launch_attn_int8(a, vq, vs, p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64), stream);
+        const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
+        // tensor-core path (u8 x s8 tcgen05.mma.kind::i8, the I8 mode of the second-generation kernel) where it takes the
+        // shape; the CUDA-core kernel otherwise -- unless the caller insisted on the tensor cores
+        n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tc2_i8(a, vq, vs, bc, stream) : 0;
+        if (n == 0 && p->kernel == BA_KERNEL_TCGEN05)
+            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 16 == 0, d <= 64, N >= 128, "
+                                            "block_cols = 64 and no bias or a dense bf16 table with 16-byte rows");
+        if (n == 0) n = ba::launch_attn_int8(a, vq, vs, bc, stream);
     } else {
         n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tcgen05(a, stream) : ba::launch_attn_simt(a, stream);
     }
@@ -563,9 +571,11 @@ static int resolve_kernel(const ba_params* p, int* kernel) {
     const char* why = "";
     const bool tc_ok = ba::tcgen05_supported(p, &why);
     int k = p->kernel;
-    if (p->quantize_pv) {  // integer P.V runs on the CUDA cores only (for now)
-        if (k == BA_KERNEL_TCGEN05) return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 has no tcgen05 kernel yet");
-        *kernel = BA_KERNEL_SIMT;
+    if (p->quantize_pv) {  // integer P.V: the tensor-core kernel where it takes the shape (decided at launch), else the CUDA cores
+        if (k != BA_KERNEL_AUTO && k != BA_KERNEL_TCGEN05 && k != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");
+        *kernel = (k != BA_KERNEL_SIMT && ba::tc2_i8_shape_ok(p->in_dtype, p->N, p->d) && tc_ok) ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
+        if (k == BA_KERNEL_TCGEN05 && *kernel != BA_KERNEL_TCGEN05)
+            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 16 == 0, d <= 64 and N >= 128");
         return BA_OK;
     }
     if (k == BA_KERNEL_AUTO) k = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
