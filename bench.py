@@ -289,6 +289,13 @@ def run_sweep(ba, device, index, quick=False):
                 ba.forward(Q, K, V, bias)
             torch.cuda.synchronize()
             n, k1, k2 = ba.profile_end()
+            # the reference's DEFAULT mode (quantize_pv = true, u8 x s8 integer P.V) where the tensor-core kernel takes the shape
+            qpv = None
+            if d % 16 == 0 and d <= 64:
+                try:
+                    qpv = tm.ms(lambda: ba.forward(Q, K, V, bias, quantize_pv=True, kernel="tcgen05"), reps=5)
+                except Exception:  # noqa: BLE001
+                    qpv = None
             dense = {}
             mask = bias.unsqueeze(0).expand(B, H, N, N) if with_bias else None
             for name, fn in dense_candidates(Q, K, V, mask).items():
@@ -304,6 +311,7 @@ def run_sweep(ba, device, index, quick=False):
             out.append({"config": tag, "B": B, "H": H, "N": N, "d": d, "bias": "dense [H,N,N] bf16" if with_bias else None,
                         "kernel": ba.select_kernel_name(B, H, N, d, torch.bfloat16, bias), "ours_ms": ours,
                         "k1_pack_ms": k1 / max(n, 1), "k2_attn_ms": k2 / max(n, 1), "ours_eff_tops": eff_ops(B, H, N, d) / ours / 1e9,
+                        "ours_quantize_pv_ms": qpv,
                         "dense_bf16_ms": dense, "dense_best": best, "dense_best_ms": ok.get(best),
                         "speedup_vs_dense_bf16": ok[best] / ours if best else None,
                         "floors_ms": s, "frac_of_floor": floor / (k2 / max(n, 1)) if n and k2 > 0 else None,

@@ -11,7 +11,7 @@ AttentionOutput binary_attention_fused_b200(const DenseMatrix& q, const DenseMat
     c.temperature = cfg.temperature;
     c.block_rows  = cfg.block_rows;                                 // validated like attention.cpp:26-28
     c.block_cols  = cfg.block_cols;
-    c.quantize_pv = cfg.quantize_pv;                                // true -> the integer P.V mode (CUDA-core kernel, K2q)
+    c.quantize_pv = cfg.quantize_pv;                                // true -> the integer P.V mode (K2b-I8 / K2q)             
     if (const auto* dense = std::get_if<DenseBias>(&cfg.bias)) {
         c.bias = dense->table;                                      // N x N table (attention.cpp:59-63)
     } else if (const auto* r1 = std::get_if<Relative1dBias>(&cfg.bias)) {

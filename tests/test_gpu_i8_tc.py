@@ -103,3 +103,14 @@ def test_tensor_core_int8_pv_full_size_c2_sample(ba, port):
         q, k, v = (x[b, h].float().cpu().numpy().astype(np.float64) for x in (Q, K, V))
         y8 = port.binary_attention_fused(q, k, v, bias=bias[h].float().cpu().numpy().astype(np.float64), quantize_pv=True, block_cols=64)[0]
         assert np.abs(O[b, h].cpu().numpy().astype(np.float64) - y8).max() <= 1e-3
+
+
+def test_tensor_core_int8_pv_long_sequence_sample(ba, port):
+    """N = 4096 (64 key blocks, the long-sequence regime of BASELINE configs[4]): one head against the oracle of the mode."""
+    import torch
+    n, d = 4096, 64
+    q, k, v, _ = make_head_inputs(port, 73, 0, n, d)
+    Q, K, V = (to_torch(x[None, None], "bf16") for x in (q, k, v))
+    O = ba.forward(Q, K, V, quantize_pv=True, kernel="tcgen05")[0, 0].cpu().numpy().astype(np.float64)
+    y8 = port.binary_attention_fused(q, k, v, quantize_pv=True, block_cols=64)[0]
+    assert np.abs(O - y8).max() <= 1e-3, np.abs(O - y8).max()
