@@ -48,6 +48,9 @@ constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16,
 #ifndef BA_PP_AT
 #define BA_PP_AT -1  // (measured: no gain with mbarriers or named barriers; kept as a dev knob) exponent pair after which a warp hands the MUFU pipe to the other query tile's pair (-1: no ping-pong)
 #endif
+#ifndef BA_EXP_LA
+#define BA_EXP_LA 0  // dev knob: software-pipeline depth (exponent pairs) of the MUFU loop; 0 = leave the schedule to ptxas
+#endif
 #ifndef BA_THR2
 #define BA_THR2 16.0f
 #endif
@@ -119,6 +122,13 @@ __device__ __forceinline__ float s32_to_float(float bits) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0,%1,%2,%3,%4,%5,%6,%7};"                        \
                  ::"r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(taddr) \
                  : "memory")
+// mbarrier test with the poll and the look at its result in different places: the predicate takes ~170 clk to land, and an
+// in-order warp that reads it at once (mbar_test) stalls for all of it -- three mbar_test in a row cost ~500 clk.  PRED is a
+// predicate register declared once at function scope (BA_DECLARE_PRED); MBAR_POLLs issued back to back share one round trip.
+#define BA_DECLARE_PRED(PRED) asm volatile(".reg .pred " #PRED ";")
+#define MBAR_POLL(PRED, bar, parity) \
+    asm volatile("mbarrier.test_wait.parity.shared::cta.b64 " #PRED ", [%0], %1;" ::"r"(smem_u32(bar)), "r"(parity) : "memory")
+#define MBAR_POLLED(PRED, out) asm volatile("selp.u32 %0, 1, 0, " #PRED ";" : "=r"(out)::"memory")
 // Per-thread constants of the softmax loop (addresses derived from %tid) are passed through this so that they live in a
 // register: left alone, the compiler re-derives them from %tid in every key tile (a dozen S2R + ~40 integer instructions
 // per tile in a loop whose issue slots are the bound).
@@ -244,6 +254,9 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             // phase), blocking waits only for what is still open.  Variants measured and rejected (same box, 16384 x 64 /
             // 16384 x 128, ms): this order 1.30 / 1.51; "P.V(t), S(t+2)" with S two tiles ahead 1.45 / 1.72 -- every softmax
             // warp then finds its S ready, all sixteen run in lock-step and sit in their MUFU-free phases together.
+            BA_DECLARE_PRED(ba_pk);
+            BA_DECLARE_PRED(ba_pv);
+            BA_DECLARE_PRED(ba_pp);
             Ring qr, kr, vr;
             uint32_t g = 0;   // key tiles of my query tile issued so far (S stage = g & 1); P.V runs one tile behind
             uint32_t up = 0;  // units of my query tile whose last P.V has been issued
@@ -256,12 +269,14 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 const uint64_t qd = q_desc + (uint64_t)((qr.stage * 2 * TM * KPAD) >> 4);
                 for (int j = 0; j < T; ++j) {
                     const uint32_t pst = (g - 1) & 1u;  // stage of the pending tile (when there is one)
-                    const uint32_t k_ok = mbar_test(&sm->kfull[kr.stage], kr.phase);
-                    uint32_t v_ok = 1, p_ok = 1;
+                    // the iteration's three barriers polled back to back (one ~170 clk round trip for all), looked at where needed
+                    uint32_t k_ok, v_ok = 1, p_ok = 1;
+                    MBAR_POLL(ba_pk, &sm->kfull[kr.stage], kr.phase);
                     if (pend) {
-                        v_ok = mbar_test(&sm->vfull[pvs], pvph);
-                        if (pact) p_ok = mbar_test(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
+                        MBAR_POLL(ba_pv, &sm->vfull[pvs], pvph);
+                        if (pact) MBAR_POLL(ba_pp, &sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
                     }
+                    MBAR_POLLED(ba_pk, k_ok);
                     if (!k_ok) mbar_wait(&sm->kfull[kr.stage], kr.phase);
                     BA_STAMP2();
                     if (act) {
@@ -287,8 +302,10 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     }
                     BA_STAMP2();
                     if (pend) {
+                        MBAR_POLLED(ba_pv, v_ok);
                         if (!v_ok) mbar_wait(&sm->vfull[pvs], pvph);
                         if (pact) {
+                            MBAR_POLLED(ba_pp, p_ok);
                             if (!p_ok) mbar_wait(&sm->pfull[X][pst], ((g - 1) >> 1) & 1u);
                             if (pj == 0 && up > 0) mbar_wait(&sm->ofree[X], (up - 1) & 1u);  // the epilogue has read the old O
                             BA_STAMP2();
@@ -631,6 +648,26 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 if (pp && (X == 1 || np > 0)) asm volatile("bar.sync %0, 128;" ::"r"(9 + quad) : "memory");
                 const float nm = -m_ref;
                 uint32_t pk[16];
+#if BA_EXP_LA > 0
+                // exponentials issued BA_EXP_LA pairs ahead of their consumers (volatile: the order is the one written), in place
+#pragma unroll
+                for (int e = 0; e < 16; ++e) fma2(x[2 * e], x[2 * e + 1], x[2 * e], x[2 * e + 1], ea, ea, nm, nm);
+#pragma unroll
+                for (int e = 0; e < 16 + BA_EXP_LA; ++e) {
+                    if (e < 16) {
+                        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[2 * e]));
+                        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[2 * e + 1]));
+                    }
+                    if (e >= BA_EXP_LA) {
+                        const int c = e - BA_EXP_LA;
+                        asm volatile("{\n\t.reg .b64 ra, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rd, {%0, %1};\n\t"
+                                     "add.rn.f32x2 rd, rd, ra;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+                                     : "+f"(l0), "+f"(l1)
+                                     : "f"(x[2 * c]), "f"(x[2 * c + 1]));
+                        pk[c] = pack_bf16(x[2 * c], x[2 * c + 1]);
+                    }
+                }
+#else
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     float a0, a1;
@@ -643,6 +680,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         ++np;
                     }
                 }
+#endif
                 BA_TMEM_ST16U(s_addr, pk);
                 BA_STAMP2();
                 tc_wait_st();
