@@ -291,7 +291,7 @@ def run_sweep(ba, device, index, quick=False):
             n, k1, k2 = ba.profile_end()
             # the reference's DEFAULT mode (quantize_pv = true, u8 x s8 integer P.V) where the tensor-core kernel takes the shape
             qpv = None
-            if d % 16 == 0 and d <= 64:
+            if d % 8 == 0 and d <= 128:
                 try:
                     qpv = tm.ms(lambda: ba.forward(Q, K, V, bias, quantize_pv=True, kernel="tcgen05"), reps=5)
                 except Exception:  # noqa: BLE001

@@ -22,7 +22,7 @@
 // !! ONE DELIBERATE DEVIATION FROM THE REFERENCE'S DEFAULTS: AttentionConfigT::quantize_pv defaults to FALSE here, the
 // reference's AttentionConfig to TRUE (attention.hpp:35).  false = fp P.V, the mode the tensor-core product path implements
 // and the one O-parity (<= 2e-3) is defined against (the reference's own int8 mode is 1.3e-3..5.5e-3
-// away from its fp64 mode); true = the reference's u8 x s8 integer P.V, here on the tensor cores for d <= 64 and on the CUDA cores beyond (same key-block
+// away from its fp64 mode); true = the reference's u8 x s8 integer P.V, here on the tensor cores for bf16 inputs (d <= 128) and on the CUDA cores otherwise (same key-block
 // semantics, within 1e-3 of the reference's result).  A caller porting `AttentionConfig::make(n, d)` who wants the
 // reference's default arithmetic must set cfg.quantize_pv = true.
 #pragma once

@@ -85,7 +85,7 @@ typedef struct {
     int32_t kernel;      /* ba_kernel */
     int32_t quantize_pv; /* AttentionConfig::quantize_pv (attention.hpp:35): 0 = fp P.V (tensor-core product path),
                             1 = the reference's default u8 x s8 integer P.V: on the tensor cores
-                            (tcgen05.mma.kind::i8, s32 accumulation per key block) for bf16 inputs with d % 16 == 0, d <= 64,
+                            (tcgen05.mma.kind::i8, s32 accumulation per key block) for bf16 inputs with d % 8 == 0, d <= 128,
                             N >= 128, block_cols = 64 and no bias or a dense bf16 table with 16-byte rows; on the CUDA cores
                             (dp4a) for every other shape.  kernel = BA_KERNEL_TCGEN05 insists on the former. */
     int32_t block_cols;  /* key-block size of the quantize_pv=1 path (AttentionConfig::block_cols, attention.cpp:50-51):

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kQvThreads) qv_amax_kernel(const void* V, int 
 }
 
 __global__ void __launch_bounds__(kQvThreads) qv_levels_kernel(const void* V, int in_dtype, int N, int d, int chunks, const double* scales,
-                                                               int8_t* vq) {
+                                                               int8_t* vq, int ldq) {
     const int head = blockIdx.x / chunks, chunk = blockIdx.x - head * chunks;
     const int cg = (d + 7) / 8, tx = threadIdx.x % cg, ty = threadIdx.x / cg, rows_per_pass = kQvThreads / cg;
     __shared__ double sdelta[256];
@@ -113,12 +113,13 @@ __global__ void __launch_bounds__(kQvThreads) qv_levels_kernel(const void* V, in
             const float fr = fabsf(xe) - floorf(fabsf(xe));
             q[i] = fabsf(fr - 0.5f) > 1e-4f ? (int8_t)__float2int_rn(xe) : (int8_t)round((double)v[i] / delta[i]);
         }
-        if (tx * 8 + 8 <= d && (off & 7) == 0) {
-            *reinterpret_cast<uint2*>(vq + off) = *reinterpret_cast<const uint2*>(q);
+        const int64_t qoff = ((int64_t)head * N + row) * ldq + tx * 8;  // level rows may be padded (ldq >= d)
+        if (tx * 8 + 8 <= d && (qoff & 7) == 0) {
+            *reinterpret_cast<uint2*>(vq + qoff) = *reinterpret_cast<const uint2*>(q);
         } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-                if (tx * 8 + i < d) vq[off + i] = q[i];
+                if (tx * 8 + i < d) vq[qoff + i] = q[i];
         }
     }
 }
@@ -130,7 +131,7 @@ __global__ void qv_scales_kernel(double* scales, int64_t n) {
     scales[i] = amax > 0.0 ? amax / 127.0 : 1.0;
 }
 
-__global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_constant__ FwdArgs a, const int8_t* __restrict__ vq,
+__global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_constant__ FwdArgs a, const int8_t* __restrict__ vq, int ldq,
                                                                    const double* __restrict__ scales, int row_blocks, int bc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ns = blockDim.y;           // 32-column slices = ceil(d/32)
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
         for (int t = tid; t < nk * w64; t += nthreads) sk[t] = a.k_words[((int64_t)head * N + j0) * w64 + t];
         for (int t = tid; t < ((nk + 3) / 4 * 4) * dp; t += nthreads) {  // byte (jj, c) lives at ((jj/4)*dp + c)*4 + jj%4
             const int jj = t / dp, c = t - jj * dp;
-            sv[((jj >> 2) * dp + c) * 4 + (jj & 3)] = (jj < nk && c < d) ? vq[((int64_t)head * N + j0 + jj) * d + c] : (int8_t)0;
+            sv[((jj >> 2) * dp + c) * 4 + (jj & 3)] = (jj < nk && c < d) ? vq[((int64_t)head * N + j0 + jj) * ldq + c] : (int8_t)0;
         }
         __syncthreads();
         if (!row_ok) continue;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kI8Rows * 8, 1) attn_int8_kernel(const __grid_
     }
 }
 
-int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, double* scales,
+int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, int ldq, double* scales,
                            cudaStream_t stream) {
     if (d > 256) return -(int)cudaErrorInvalidValue;
     if (heads == 0 || N == 0) return 0;
@@ -231,19 +232,19 @@ int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, in
     cudaError_t e = cudaMemsetAsync(scales, 0, (size_t)heads * d * sizeof(double), stream);
     if (e != cudaSuccess) return -(int)e;
     qv_amax_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales);
-    qv_levels_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales, vq);
+    qv_levels_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales, vq, ldq);
     qv_scales_kernel<<<(unsigned)((heads * d + 255) / 256), 256, 0, stream>>>(scales, heads * d);
     e = cudaGetLastError();
     return e == cudaSuccess ? 3 : -(int)e;
 }
 
-int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream) {
+int launch_attn_int8(const FwdArgs& a, const int8_t* vq, int ldq, const double* scales, int block_cols, cudaStream_t stream) {
     const int ns = (a.d + kI8Slice - 1) / kI8Slice;
     if (ns > 8 || a.W64 > kI8MaxW64 || block_cols < 1 || block_cols > kI8MaxBc) return -(int)cudaErrorInvalidValue;
     const int row_blocks = (a.N + kI8Rows - 1) / kI8Rows;
     const dim3 block(kI8Rows, ns);
     const size_t smem = (size_t)kI8MaxBc * ns * kI8Slice + sizeof(uint64_t) * kI8MaxBc * a.W64;  // s8 tile + packed K words
-    attn_int8_kernel<<<(unsigned)(a.BH * row_blocks), block, smem, stream>>>(a, vq, scales, row_blocks, block_cols);
+    attn_int8_kernel<<<(unsigned)(a.BH * row_blocks), block, smem, stream>>>(a, vq, ldq, scales, row_blocks, block_cols);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 1 : -(int)e;
 }

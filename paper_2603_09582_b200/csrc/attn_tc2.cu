@@ -12,27 +12,35 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 EncodeTiledFn get_encode_fn();  // attn_tcgen05.cu
 }  // namespace tc
 
-static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vscales, int32_t* dbg_S, int dbg_head, long long* dbg_T,
-                          cudaStream_t stream);
+static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, int ldq, int vcol0, const double* vscales, int32_t* dbg_S, int dbg_head,
+                          long long* dbg_T, cudaStream_t stream);
 
 // Returns the number of kernels launched (> 0), a negative cudaError_t, or 0 when this kernel does not take the shape
 // (the caller then runs the first-generation kernel).
 int launch_attn_tc2(const FwdArgs& a, int32_t* dbg_S, int dbg_head, long long* dbg_T, cudaStream_t stream) {
-    return launch_tc2_any(a, nullptr, nullptr, dbg_S, dbg_head, dbg_T, stream);
+    return launch_tc2_any(a, nullptr, 0, 0, nullptr, dbg_S, dbg_head, dbg_T, stream);
 }
 
 // quantize_pv = true on the tensor cores (the I8 mode of attn_tc2_kernel): vq = s8 value levels [BH, N, d], vscales = their
-// per-channel fp64 scales [BH, d] (K1v).  Takes block_cols = 64 (one key tile per block, the reference's default for N >= 64),
-// bf16-packed inputs with d % 16 == 0, d <= 64, N >= 128 and no bias or a TMA-able dense bf16 table; 0 otherwise (the caller
-// then runs the CUDA-core kernel).
-int launch_attn_tc2_i8(const FwdArgs& a, const int8_t* vq, const double* vscales, int block_cols, cudaStream_t stream) {
+// per-channel fp64 scales [BH, d] (K1v), level rows ldq bytes apart (a multiple of 16).  Takes block_cols = 64 (one key tile per
+// block, the reference's default for N >= 64), bf16-packed inputs with d % 8 == 0, d <= 128, N >= 128 and no bias or a TMA-able
+// dense bf16 table; 0 otherwise (the caller then runs the CUDA-core kernel).  The fp32 O and the s32 block accumulator of a
+// query tile share 128 TMEM columns, so one launch covers 64 columns of V: wider heads take a second pass over the other
+// columns (logits and weights recomputed).
+int launch_attn_tc2_i8(const FwdArgs& a, const int8_t* vq, int ldq, const double* vscales, int block_cols, cudaStream_t stream) {
     if (tc::env_long("BA_TC2_I8", 1) == 0 || block_cols != 64 || !vq || !vscales) return 0;
-    if (!tc2_i8_shape_ok(a.in_dtype, a.N, a.d) || reinterpret_cast<uintptr_t>(vq) % 16 != 0) return 0;
-    return launch_tc2_any(a, vq, vscales, nullptr, 0, nullptr, stream);
+    if (!tc2_i8_shape_ok(a.in_dtype, a.N, a.d) || reinterpret_cast<uintptr_t>(vq) % 16 != 0 || ldq % 16 != 0) return 0;
+    int total = 0;
+    for (int c0 = 0; c0 < a.d; c0 += 64) {
+        const int n = launch_tc2_any(a, vq, ldq, c0, vscales, nullptr, 0, nullptr, stream);
+        if (n <= 0) return c0 == 0 ? n : -(int)cudaErrorUnknown;  // (the gate is the same for every slice)
+        total += n;
+    }
+    return total;
 }
 
-static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vscales, int32_t* dbg_S, int dbg_head, long long* dbg_T,
-                          cudaStream_t stream) {
+static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, int ldq, int vcol0, const double* vscales, int32_t* dbg_S, int dbg_head,
+                          long long* dbg_T, cudaStream_t stream) {
     using namespace tc2;
     const bool i8 = vq != nullptr;
     if (env_long("BA_TC2", 1) == 0 && !i8) return 0;
@@ -67,8 +75,10 @@ static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vsca
         prm.units = std::min(a.unit1, a.BH * prm.ublocks);
         if (prm.units <= prm.unit0) return 0;
     }
-    prm.dvp = (a.d + 15) / 16 * 16;
-    prm.nbox = (a.d + 63) / 64;
+    prm.vcol0 = vcol0;
+    prm.dsl = i8 ? std::min(64, a.d - vcol0) : a.d;
+    prm.dvp = (prm.dsl + 15) / 16 * 16;
+    prm.nbox = (prm.dsl + 63) / 64;
     prm.dbg_S = dbg_S;
     prm.dbg_head = dbg_head;
     prm.g = g;
@@ -97,7 +107,7 @@ static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vsca
     const cuuint32_t estr[3] = {1, 1, 1};
     if (i8) {  // s8 value levels [BH, N, d]: boxes of 64 keys x 64 channels (64 B rows, 64B swizzle; channels past d read as 0)
         const cuuint64_t gdim[3] = {(cuuint64_t)a.d, (cuuint64_t)a.N, (cuuint64_t)a.BH};
-        const cuuint64_t gstr[2] = {(cuuint64_t)a.d, (cuuint64_t)a.N * a.d};
+        const cuuint64_t gstr[2] = {(cuuint64_t)ldq, (cuuint64_t)a.N * ldq};
         const cuuint32_t box[3] = {64, (cuuint32_t)TN, 1};
         if (enc(&vmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(vq), gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -135,7 +145,15 @@ static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, const double* vsca
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -(int)cudaErrorInvalidValue;
     }
-    if (i8) return kpad == 32 ? launch_i8<32>(prm, bias_mode, vmap, bmap, omap, stream) : launch_i8<64>(prm, bias_mode, vmap, bmap, omap, stream);
+    if (i8) {
+        switch (kpad) {
+            case 32: return launch_i8<32>(prm, bias_mode, vmap, bmap, omap, stream);
+            case 64: return launch_i8<64>(prm, bias_mode, vmap, bmap, omap, stream);
+            case 96: return launch_i8<96>(prm, bias_mode, vmap, bmap, omap, stream);
+            case 128: return launch_i8<128>(prm, bias_mode, vmap, bmap, omap, stream);
+        }
+        return 0;
+    }
     switch (kpad) {
         case 32: return launch_kpad2<32>(prm, bias_mode, vmap, bmap, omap, stream);
         case 64: return launch_kpad2<64>(prm, bias_mode, vmap, bmap, omap, stream);

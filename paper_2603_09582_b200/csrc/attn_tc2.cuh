@@ -87,6 +87,7 @@ struct Params2 {
     int g;         // BIAS 4: grid side sqrt(N) (a multiple of 32)
     int vbox;      // bytes of one V box in shared memory (kVBox, or kVBox8 in the I8 mode)
     const double* vscales;  // I8: [BH, d] per-channel value scales (quantize_values, quantize.cpp:57-74)
+    int vcol0, dsl;         // I8: this launch computes O columns [vcol0, vcol0 + dsl) (dsl <= 64; wider heads take one pass per slice)
     int32_t* dbg_S;
     int dbg_head;
     long long* dbg_T;
@@ -403,7 +404,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                         mbar_wait(&sm->vfree[vr.stage], vr.phase ^ 1u);
                         mbar_expect_tx(&sm->vfull[vr.stage], prm.nbox * prm.vbox);
                         for (int b = 0; b < prm.nbox; ++b)
-                            tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * prm.vbox, b * 64, j * TN, head);
+                            tma_load_3d(&vmap, &sm->vfull[vr.stage], sV + (vr.stage * prm.nbox + b) * prm.vbox, (I8 ? prm.vcol0 : 0) + b * 64, j * TN, head);
                         vr.next(prm.vst);
                     }
                 }
@@ -694,8 +695,9 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
             pair_sync(pair_id);
             const float l = (l0 + l1) + sm->xch[X][half ^ 1][r];
             const float inv_l = I8 ? 1.0f / l / 255.0f : 1.0f / l;
-            float* orow = a.O + ((int64_t)head * N + row) * d;
-            __nv_bfloat16* orow16 = reinterpret_cast<__nv_bfloat16*>(a.O) + ((int64_t)head * N + row) * d;  // (out_bf16)
+            const int vc0 = I8 ? prm.vcol0 : 0, dcols = I8 ? prm.dsl : d;  // I8: this pass owns O columns [vc0, vc0 + dcols)
+            float* orow = a.O + ((int64_t)head * N + row) * d + vc0;
+            __nv_bfloat16* orow16 = reinterpret_cast<__nv_bfloat16*>(a.O) + ((int64_t)head * N + row) * d + vc0;  // (out_bf16)
             for (int c = oc0; c < oc1; c += 16) {
                 float o[16], of[16];
                 BA_TMEM_LD16(o_addr + c, o, 0);
@@ -705,12 +707,12 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     __syncwarp();
                 }
                 tc_wait_ld();
-                if (I8) {  // O = (O * rescale(last) + acc(last)) / l / 255 * delta[c]  (attention.cpp:338-343, 361-363); d % 16 == 0
-                    const double* dl = prm.vscales + (int64_t)head * d + c;
+                if (I8) {  // O = (O * rescale(last) + acc(last)) / l / 255 * delta[c]  (attention.cpp:338-343, 361-363)
+                    const double* dl = prm.vscales + (int64_t)head * d + vc0 + c;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const float acc = s32_to_float(o[i]);
-                        o[i] = (T > 1 ? fmaf(of[i], rs_prev, acc) : acc) * inv_l * (float)__ldg(dl + i);
+                        o[i] = (T > 1 ? fmaf(of[i], rs_prev, acc) : acc) * inv_l * (c + i < dcols ? (float)__ldg(dl + i) : 0.f);
                     }
                 } else {
 #pragma unroll
@@ -735,20 +737,20 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_3d(&omap, box, c, row - lane, head);
+                        tma_store_3d(&omap, box, vc0 + c, row - lane, head);
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 } else if (row < N) {
                     if (a.out_bf16) {
 #pragma unroll
                         for (int q = 0; q < 2; ++q)
-                            if (c + 8 * q + 8 <= d)
+                            if (c + 8 * q + 8 <= dcols)
                                 *reinterpret_cast<uint4*>(orow16 + c + 8 * q) =
                                     make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
                                                pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
                     } else {
-                        if (c + 8 <= d) stg_256(orow + c, o);
-                        if (c + 16 <= d) stg_256(orow + c + 8, o + 8);
+                        if (c + 8 <= dcols) stg_256(orow + c, o);
+                        if (c + 16 <= dcols) stg_256(orow + c + 8, o + 8);
                     }
                 }
             }
@@ -880,10 +882,11 @@ static int launch_main2(const Params2& prm, int bias_mode, const CUtensorMap& vm
     return launch_variant2<KPAD, 0, false>(prm, vmap, bmap, omap, stream);
 }
 
-// I8 mode (quantize_pv = true on the tensor cores): d <= 64, so KPAD is 32 or 64; bias none or the dense bf16 TMA table.
+// I8 mode (quantize_pv = true on the tensor cores): bias none or the dense bf16 TMA table; one launch per 64-column slice of V
+// (prm.vcol0 / prm.dsl), the plane expansion before the first one only.
 template <int KPAD>
 static int launch_i8(const Params2& prm, int bias_mode, const CUtensorMap& vmap, const CUtensorMap& bmap, const CUtensorMap& omap, cudaStream_t stream) {
-    const int ne = launch_expand_qk<KPAD>(prm.a, prm.tiles, prm.ublocks, stream);
+    const int ne = prm.vcol0 == 0 ? launch_expand_qk<KPAD>(prm.a, prm.tiles, prm.ublocks, stream) : 0;
     if (ne < 0) return ne;
     int nk;
     if (prm.a.N % TN != 0)

@@ -49,11 +49,12 @@ int launch_pack_signs(const void* X, int in_dtype, int64_t heads, int N, int d, 
 int pack_partials_per_head(int N, int d, int in_dtype);
 int launch_binary_logits(const uint64_t* qw, const uint64_t* kw, int N, int d, int32_t* S, cudaStream_t stream);
 int launch_attn_simt(const FwdArgs& a, cudaStream_t stream);
-int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, double* scales,
+int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, int d, int8_t* vq, int ldq, double* scales,
                            cudaStream_t stream);
-int launch_attn_int8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream);
+int launch_attn_int8(const FwdArgs& a, const int8_t* vq, int ldq, const double* scales, int block_cols, cudaStream_t stream);
+inline int i8_level_ld(int d) { return (d + 15) / 16 * 16; }  // row stride of the workspace's s8 level plane: 16-byte multiples for TMA
 int launch_attn_tcgen05(const FwdArgs& a, cudaStream_t stream);
-int launch_attn_tc2_i8(const FwdArgs& a, const int8_t* vq, const double* scales, int block_cols, cudaStream_t stream);  // 0: shape not taken
+int launch_attn_tc2_i8(const FwdArgs& a, const int8_t* vq, int ldq, const double* scales, int block_cols, cudaStream_t stream);  // 0: shape not taken
 // Shapes the second-generation tcgen05 kernel (attn_tc2.cuh) takes; decides whether the workspace carries the expanded K plane.
 inline bool tc2_shape_ok(int in_dtype, int N, int d) {
     const char* e = getenv("BA_TC2_MIN_N");  // dev knob; default: below ~512 keys the first-generation kernel is faster (measured)
@@ -62,7 +63,8 @@ inline bool tc2_shape_ok(int in_dtype, int N, int d) {
 }
 // Shapes the I8 mode of that kernel takes (quantize_pv = true on the tensor cores): the s32 accumulator and the fp32 O share the
 // 256 TMEM columns of a query tile with the two S stages, and the s8 value rows must be 16-byte multiples for TMA.
-inline bool tc2_i8_shape_ok(int in_dtype, int N, int d) { return in_dtype == BA_BF16 && d % 16 == 0 && d <= 64 && N >= 128; }
+// Heads wider than 64 run one pass per 64-column slice of V (the logits and weights are recomputed: they are the cheap half).
+inline bool tc2_i8_shape_ok(int in_dtype, int N, int d) { return in_dtype == BA_BF16 && d % 8 == 0 && d <= 128 && N >= 128; }
 inline size_t tc2_kexp_bytes(int64_t heads, int N, int d) {  // whole 64-key tiles per head
     return (size_t)heads * ((N + 63) / 64 * 64) * ((d + 31) / 32 * 32);
 }

@@ -66,7 +66,7 @@ Layout make_layout(const ba_params* p, int64_t heads = -1) {
     L.partials = off; off += align_up(2 * (size_t)L.BH * L.chunks * sizeof(float), 256);
     L.vq = L.vscales = off;
     if (p->quantize_pv) {  // s8 levels of V and their per-channel fp64 scales (quantize_values)
-        L.vq = off; off += align_up((size_t)L.BH * p->N * p->d, 256);
+        L.vq = off; off += align_up((size_t)L.BH * p->N * ba::i8_level_ld(p->d), 256);  // rows padded to 16 bytes (TMA)
         L.vscales = off; off += align_up((size_t)L.BH * p->d * sizeof(double), 256);
     }
     L.kexp = off;  // expanded K plane of the second-generation tcgen05 kernel (e4m3 +-1.0 bytes, UMMA tile order)
@@ -360,7 +360,7 @@ int ba_quantize_values(ba_handle* h, const ba_params* p, const void* V, int8_t* 
     if (!V || !vq || !scales) return fail(BA_ERR_SHAPE, "quantize_values: V, vq and scales must be non-NULL");
     if (p->d > 256) return fail(BA_ERR_UNSUPPORTED, "head dim %d > 256 is not supported", p->d);
     BA_BIND_DEVICE(h);
-    const int n = ba::launch_quantize_values(V, p->in_dtype, (int64_t)p->B * p->H, p->N, p->d, vq, scales,
+    const int n = ba::launch_quantize_values(V, p->in_dtype, (int64_t)p->B * p->H, p->N, p->d, vq, p->d, scales,
                                              static_cast<cudaStream_t>(stream));
     if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
     h->launches += n;
@@ -544,17 +544,18 @@ static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0
     if (p->quantize_pv) {  // the reference's default mode: s8 V levels (K1v), then the integer P.V kernel
         int8_t* vq = reinterpret_cast<int8_t*>(ws + L.vq);
         double* vs = reinterpret_cast<double*>(ws + L.vscales);
-        n = ba::launch_quantize_values(V, p->in_dtype, heads, p->N, p->d, vq, vs, stream);
+        const int ldq = ba::i8_level_ld(p->d);
+        n = ba::launch_quantize_values(V, p->in_dtype, heads, p->N, p->d, vq, ldq, vs, stream);
         if (n < 0) return fail(BA_ERR_CUDA, "quantize_values launch: %s", cudaGetErrorString((cudaError_t)(-n)));
         h->launches += n;
         const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
         // tensor-core path (u8 x s8 tcgen05.mma.kind::i8, the I8 mode of the second-generation kernel) where it takes the
         // shape; the CUDA-core kernel otherwise -- unless the caller insisted on the tensor cores
-        n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tc2_i8(a, vq, vs, bc, stream) : 0;
+        n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tc2_i8(a, vq, ldq, vs, bc, stream) : 0;
         if (n == 0 && p->kernel == BA_KERNEL_TCGEN05)
-            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 16 == 0, d <= 64, N >= 128, "
+            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 8 == 0, d <= 128, N >= 128, "
                                             "block_cols = 64 and no bias or a dense bf16 table with 16-byte rows");
-        if (n == 0) n = ba::launch_attn_int8(a, vq, vs, bc, stream);
+        if (n == 0) n = ba::launch_attn_int8(a, vq, ldq, vs, bc, stream);
     } else {
         n = kernel == BA_KERNEL_TCGEN05 ? ba::launch_attn_tcgen05(a, stream) : ba::launch_attn_simt(a, stream);
     }
@@ -575,7 +576,7 @@ static int resolve_kernel(const ba_params* p, int* kernel) {
         if (k != BA_KERNEL_AUTO && k != BA_KERNEL_TCGEN05 && k != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");
         *kernel = (k != BA_KERNEL_SIMT && ba::tc2_i8_shape_ok(p->in_dtype, p->N, p->d) && tc_ok) ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
         if (k == BA_KERNEL_TCGEN05 && *kernel != BA_KERNEL_TCGEN05)
-            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 16 == 0, d <= 64 and N >= 128");
+            return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 8 == 0, d <= 128 and N >= 128");
         return BA_OK;
     }
     if (k == BA_KERNEL_AUTO) k = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;

@@ -42,7 +42,8 @@ def ref_qpv(Q, K, V, bias, scale, bc=64):
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 if mode in ("all", "check"):
     for (B, H, N, d, wb) in [(1, 2, 128, 64, False), (1, 2, 256, 64, True), (2, 3, 197, 64, True), (1, 2, 577, 64, False),
-                             (1, 2, 1024, 32, False), (1, 2, 512, 48, True), (1, 3, 320, 16, True), (1, 2, 2048, 64, True)]:
+                             (1, 2, 1024, 32, False), (1, 2, 512, 48, True), (1, 3, 320, 16, True), (1, 2, 2048, 64, True),
+                             (1, 2, 256, 72, True), (2, 2, 1024, 72, False), (1, 2, 384, 128, True), (1, 2, 577, 96, False), (1, 2, 130, 104, True)]:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
         bias = (0.5 * torch.randn(H, N, (N + 7) // 8 * 8, device="cuda")).to(torch.bfloat16)[:, :, :N] if wb else None
         scale = 1.0 / d ** 0.5
@@ -56,7 +57,7 @@ if mode in ("all", "check"):
         print(f"B{B} H{H} N{N} d{d} bias={wb}: max|O-ref| cuda-core {e1:.2e}  tensor-core {e2:.2e}  |tc-cc| {(o1 - o2).abs().max().item():.2e}"
               f"  stats dm {(m1 - m2).abs().max().item():.1e} dl/l {((l1 - l2).abs() / l1).max().item():.1e}  nan={bool(torch.isnan(o2).any())}", flush=True)
 if mode in ("all", "time"):
-    for (B, H, N, d) in [(256, 12, 197, 64), (64, 12, 577, 64), (1, 16, 4096, 64), (1, 16, 16384, 64)]:
+    for (B, H, N, d) in [(256, 12, 197, 64), (64, 12, 577, 64), (32, 16, 1024, 72), (1, 16, 4096, 64), (1, 16, 4096, 128), (1, 16, 16384, 64)]:
         Q, K, V = (torch.randn(B, H, N, d, device="cuda").to(torch.bfloat16) for _ in range(3))
         bias = (0.5 * torch.randn(H, N, (N + 7) // 8 * 8, device="cuda")).to(torch.bfloat16)[:, :, :N]
         res = {}

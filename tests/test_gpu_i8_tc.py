@@ -21,7 +21,8 @@ def ba():
 
 
 @pytest.mark.parametrize("bias_mode", [None, "per_head"])
-@pytest.mark.parametrize("n,d", [(197, 64), (577, 64), (128, 16), (256, 32), (384, 48), (1024, 64), (130, 64), (639, 32)])
+@pytest.mark.parametrize("n,d", [(197, 64), (577, 64), (128, 16), (256, 32), (384, 48), (1024, 64), (130, 64), (639, 32),
+                                 (256, 72), (1024, 72), (384, 128), (130, 104), (256, 40), (577, 96)])  # d > 64: one pass per 64 columns of V
 def test_tensor_core_int8_pv_matches_reference_default(ba, port, n, d, bias_mode):
     heads = [make_head_inputs(port, 71, s, n, d, bias_scale=0.5 if bias_mode else None) for s in range(2)]
     Q, K, V = (to_torch(np.stack([h[i] for h in heads])[None], "bf16") for i in range(3))
@@ -64,8 +65,9 @@ def test_tensor_core_int8_pv_dispatch(ba, monkeypatch):
     assert torch.equal(ba.forward(Q, K, V, quantize_pv=True), cc)
     monkeypatch.delenv("BA_TC2_I8")
     assert torch.equal(ba.forward(Q, K, V, quantize_pv=True, block_cols=32), ba.forward(Q, K, V, quantize_pv=True, block_cols=32, kernel="simt"))
-    for shape in ((1, 1, 256, 72), (1, 1, 256, 128), (1, 1, 96, 64), (1, 1, 256, 40)):
-        x = torch.randn(*shape, device="cuda").to(torch.bfloat16)
+    for shape, dt in (((1, 1, 96, 64), torch.bfloat16), ((1, 1, 256, 20), torch.bfloat16), ((1, 1, 256, 160), torch.bfloat16),
+                      ((1, 1, 256, 64), torch.float32)):
+        x = torch.randn(*shape, device="cuda").to(dt)
         ba.forward(x, x, x, quantize_pv=True)  # auto: the CUDA-core kernel
         with pytest.raises(pkg.UnsupportedError):
             ba.forward(x, x, x, quantize_pv=True, kernel="tcgen05")
@@ -76,7 +78,14 @@ def test_tensor_core_int8_pv_dispatch(ba, monkeypatch):
 def test_tensor_core_int8_pv_shards_and_bf16_output(ba):
     import torch
     g = torch.Generator(device="cuda").manual_seed(5)
-    Q, K, V = (torch.randn(1, 3, 700, 64, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    _shards_and_bf16(ba, 64)
+    _shards_and_bf16(ba, 72)
+
+
+def _shards_and_bf16(ba, d):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Q, K, V = (torch.randn(1, 3, 700, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
     bias = (0.5 * torch.randn(3, 700, 704, device="cuda", generator=g)).to(torch.bfloat16)[:, :, :700]
     whole = ba.forward(Q, K, V, bias, quantize_pv=True, kernel="tcgen05")
     out = torch.zeros_like(whole)
