@@ -124,6 +124,66 @@ __global__ void __launch_bounds__(kQvThreads) qv_levels_kernel(const void* V, in
     }
 }
 
+// Heads of at most one chunk (N <= 256: the ViT shapes): the three steps in ONE launch, one CTA per head -- the second pass
+// over the head's 25-50 KB comes out of L1 / L2, and nothing goes through global atomics.
+__global__ void __launch_bounds__(kQvThreads) qv_head_kernel(const void* V, int in_dtype, int N, int d, double* scales, int8_t* vq, int ldq) {
+    __shared__ unsigned int amax_bits[256];
+    __shared__ double sdelta[256];
+    __shared__ float srdelta[256];
+    const int head = blockIdx.x;
+    const int cg = (d + 7) / 8, tx = threadIdx.x % cg, ty = threadIdx.x / cg, rows_per_pass = kQvThreads / cg;
+    for (int c = threadIdx.x; c < 256; c += kQvThreads) amax_bits[c] = 0u;
+    __syncthreads();
+    if (ty < rows_per_pass) {
+        float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int row = ty; row < N; row += rows_per_pass) {
+            float v[8];
+            qv_load8(V, in_dtype, ((int64_t)head * N + row) * d + tx * 8, tx * 8, d, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], fabsf(v[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (tx * 8 + i < d) atomicMax(&amax_bits[tx * 8 + i], __float_as_uint(m[i]));
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 256; c += kQvThreads) {
+        const double amax = c < d ? (double)__uint_as_float(amax_bits[c]) : 0.0;
+        const double dl = amax > 0.0 ? amax / 127.0 : 1.0;  // quantize.cpp:61-66
+        sdelta[c] = dl;
+        srdelta[c] = (float)(1.0 / dl);
+        if (c < d) scales[(int64_t)head * d + c] = dl;
+    }
+    __syncthreads();
+    if (ty >= rows_per_pass) return;
+    double delta[8];
+    float rdelta[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        delta[i] = sdelta[(tx * 8 + i) & 255];
+        rdelta[i] = srdelta[(tx * 8 + i) & 255];
+    }
+    for (int row = ty; row < N; row += rows_per_pass) {
+        float v[8];
+        qv_load8(V, in_dtype, ((int64_t)head * N + row) * d + tx * 8, tx * 8, d, v);
+        int8_t q[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // as in qv_levels_kernel
+            const float xe = v[i] * rdelta[i];
+            const float fr = fabsf(xe) - floorf(fabsf(xe));
+            q[i] = fabsf(fr - 0.5f) > 1e-4f ? (int8_t)__float2int_rn(xe) : (int8_t)round((double)v[i] / delta[i]);
+        }
+        const int64_t qoff = ((int64_t)head * N + row) * ldq + tx * 8;
+        if (tx * 8 + 8 <= d && (qoff & 7) == 0) {
+            *reinterpret_cast<uint2*>(vq + qoff) = *reinterpret_cast<const uint2*>(q);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (tx * 8 + i < d) vq[qoff + i] = q[i];
+        }
+    }
+}
+
 __global__ void qv_scales_kernel(double* scales, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -229,6 +289,11 @@ int launch_quantize_values(const void* V, int in_dtype, int64_t heads, int N, in
     if (d > 256) return -(int)cudaErrorInvalidValue;
     if (heads == 0 || N == 0) return 0;
     const int chunks = (N + kQvChunk - 1) / kQvChunk;
+    if (chunks == 1) {
+        qv_head_kernel<<<(unsigned)heads, kQvThreads, 0, stream>>>(V, in_dtype, N, d, scales, vq, ldq);
+        const cudaError_t e1 = cudaGetLastError();
+        return e1 == cudaSuccess ? 1 : -(int)e1;
+    }
     cudaError_t e = cudaMemsetAsync(scales, 0, (size_t)heads * d * sizeof(double), stream);
     if (e != cudaSuccess) return -(int)e;
     qv_amax_kernel<<<(unsigned)(heads * chunks), kQvThreads, 0, stream>>>(V, in_dtype, N, d, chunks, scales);
