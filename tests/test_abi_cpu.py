@@ -62,6 +62,30 @@ def test_workspace_and_param_validation(lib):
     assert lib.ba_workspace_bytes(C.byref(p)) == 0
 
 
+def test_ctypes_mirror_matches_the_header_field_for_field(tmp_path):
+    """api._Params must be include/binattn_cuda.h's ba_params: same field names in the same order, same offsets and total
+    size (a compiled probe prints offsetof for every field the header declares)."""
+    import re
+    import subprocess
+    from paper_2603_09582_b200.api import _Params
+    hdr = open(os.path.join(ROOT, "include", "binattn_cuda.h")).read()
+    body = hdr[hdr.index("typedef struct {", hdr.index("ba_bias_mode")):hdr.index("} ba_params;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in re.findall(r"(?:int32_t|int64_t|float)\s+([^;]+);", body):
+        names += [n.strip() for n in decl.split(",")]
+    assert names == [f[0] for f in _Params._fields_]
+    src = tmp_path / "probe.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "binattn_cuda.h"\nint main(void){'
+                   + "".join(f'printf("%zu\\n", offsetof(ba_params, {n}));' for n in names)
+                   + 'printf("%zu\\n", sizeof(ba_params));return 0;}')
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert vals[:-1] == [getattr(_Params, n).offset for n in names]
+    assert vals[-1] == C.sizeof(_Params)
+
+
 def test_shard_range_matches_python_and_covers(lib):
     from paper_2603_09582_b200 import shard_range
     for total in (0, 1, 6, 16, 512, 3072, 3073):
