@@ -114,10 +114,16 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
         : "memory");
 }
-// s32 accumulator word (arrived through a float register) -> float, exactly, for |v| < 2^22 (a tile's P.V is at most
-// 64 * 255 * 127 < 2^21): integer add into the mantissa of 1.5 * 2^23, then subtract it -- ALU + FMA pipe instead of I2F.
+// s32 accumulator word (arrived through a float register) -> float.  I2F runs on the conversion unit that shares the
+// 16-per-clock pipe with ex2; the alternative that stays off it -- integer add into the mantissa of 1.5 * 2^23, then subtract
+// it, exact below 2^22 -- costs two issue slots instead of one, and the I8 loop is bound by issue slots, not by that pipe
+// (measured: I2F 2.5 % faster at N = 16384).  BA_I8_MAGIC selects the other one.
 __device__ __forceinline__ float s32_to_float(float bits) {
+#ifdef BA_I8_MAGIC
     return __int_as_float(__float_as_int(bits) + 0x4B400000) - 12582912.0f;
+#else
+    return (float)__float_as_int(bits);
+#endif
 }
 #define BA_TMEM_ST8U(taddr, v)                                                                                  \
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0,%1,%2,%3,%4,%5,%6,%7};"                        \
