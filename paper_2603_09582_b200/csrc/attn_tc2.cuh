@@ -29,6 +29,11 @@
 // maxima only when the flag is up (always on the first tile of a unit).  Without a bias every logit is bounded a priori by
 // |x| <= d*mu_q*mu_k/tau, so when that bound is below 2^32 the reference is the bound itself and the kernel computes no
 // row max at all (FAST path; the row_max / row_sum outputs need the true max and take the general path).
+//
+// I8 mode (template parameter; quantize_pv = true, the reference's default arithmetic, attention.cpp:332-343, 361-363): the
+// same pipeline with an integer P.V half -- u8 weights relative to the TRUE running max of every 64-key block as A operand in
+// tensor memory, s8 value levels as MN-major B operand, tcgen05.mma.kind::i8 into a fresh s32 accumulator per tile that the
+// softmax threads fold into an fp32 O (also in tensor memory) one tile later.  See the comment at the kernel.
 #pragma once
 #include "attn_tcgen05.cuh"
 
