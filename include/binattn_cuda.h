@@ -100,6 +100,9 @@ typedef struct {
                             [B,H,N,d] -- the fp32 result rounded to nearest-even in the kernel's epilogue, i.e. exactly
                             what converting the fp32 output afterwards gives, without the fp32 round trip through HBM.
                             The O argument then points to bf16 storage.  row_max / row_sum stay float32. */
+    int32_t bias_on_device; /* ba_binary_attention_host only: 1 = `bias` is already a DEVICE pointer (the table is a model
+                            parameter uploaded once, not an input of every call); Q, K, V and O stay host buffers.  0 = the
+                            table is copied from host memory in every call like the other inputs. */
 } ba_params;
 
 #define BA_UNIT_ROWS 256 /* query rows of one shard unit (one unit of the second-generation kernel, two of the first's) */

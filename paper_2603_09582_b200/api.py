@@ -53,7 +53,7 @@ class _Params(C.Structure):
                 ("bias_mode", C.c_int32), ("bias_heads", C.c_int32), ("bias_dtype", C.c_int32),
                 ("bias_ld", C.c_int64), ("inv_tau", C.c_float), ("kernel", C.c_int32),
                 ("quantize_pv", C.c_int32), ("block_cols", C.c_int32), ("unit_begin", C.c_int64), ("unit_end", C.c_int64),
-                ("out_bf16", C.c_int32)]
+                ("out_bf16", C.c_int32), ("bias_on_device", C.c_int32)]
 
 
 _lib = None
@@ -404,9 +404,10 @@ class BinaryAttention:
         B, H, N, d = Q.shape
         Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
         bias, bias_t = self._check_bias(bias, H, N)
-        if bias_t is not None and not isinstance(bias, (Relative1dBias, Relative2dBias)):
+        if bias_t is not None and not isinstance(bias, (Relative1dBias, Relative2dBias)) and not bias_t.is_cuda:
             bias = bias_t = bias_t.contiguous()
         p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        p.bias_on_device = 1 if (bias_t is not None and bias_t.is_cuda) else 0  # a table that already lives on the GPU (a model parameter)
         if out_dtype not in (torch.float32, torch.bfloat16):
             raise ValidationError("out_dtype must be torch.float32 or torch.bfloat16")
         p.out_bf16 = 1 if out_dtype == torch.bfloat16 else 0

@@ -123,6 +123,7 @@ int check_params(const ba_params* p, bool need_attention) {
                         (long long)p->unit_end, (long long)total);
     }
     if (p->out_bf16 != 0 && p->out_bf16 != 1) return fail(BA_ERR_VALIDATION, "out_bf16 must be 0 (float32 O) or 1 (bfloat16 O)");
+    if (p->bias_on_device != 0 && p->bias_on_device != 1) return fail(BA_ERR_VALIDATION, "bias_on_device must be 0 or 1");
     if (p->quantize_pv) {
         const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
         if (bc < 1 || bc > p->N)  // attention.cpp:26-28
@@ -689,7 +690,8 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     size_t per = 0;  // largest chunk (workspace slices are sized for it)
     for (int c = 0; c < chunks; ++c) per = std::max(per, plan[c]);
     const Layout Lc = make_layout(p, (int64_t)per);
-    const size_t need[8] = {BH * head_in, BH * head_in, BH * head_in, bias_bytes, BH * head_out,
+    const bool bias_dev = p->bias_on_device != 0 && bias_bytes;  // the table already lives on this device
+    const size_t need[8] = {BH * head_in, BH * head_in, BH * head_in, bias_dev ? 0 : bias_bytes, BH * head_out,
                             row_max ? BH * head_row : 0, row_sum ? BH * head_row : 0, (size_t)chunks * Lc.total};
     for (int i = 0; i < 8; ++i)
         if (need[i] && (rc = ensure(&h->stage[i], &h->stage_bytes[i], need[i], false))) return rc;
@@ -700,7 +702,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     char* const dO = static_cast<char*>(h->stage[4]);
     char* const dM = static_cast<char*>(h->stage[5]);
     char* const dL = static_cast<char*>(h->stage[6]);
-    if (bias_bytes) BA_CUDA(cudaMemcpyAsync(h->stage[3], bias, bias_bytes, cudaMemcpyHostToDevice, h->stream_in));
+    if (bias_bytes && !bias_dev) BA_CUDA(cudaMemcpyAsync(h->stage[3], bias, bias_bytes, cudaMemcpyHostToDevice, h->stream_in));
     size_t h0 = 0;
     for (int c = 0; c < chunks; h0 += plan[c], ++c) {
         const size_t nh = plan[c];
@@ -713,7 +715,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
         BA_CUDA(cudaEventRecord(h->ev_in[c], h->stream_in));
         BA_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
         rc = fwd_range(h, p, kernel, (int64_t)h0, (int64_t)nh, dQ + h0 * head_in, dK + h0 * head_in, dV + h0 * head_in,
-                       bias_bytes ? h->stage[3] : nullptr, dO + h0 * head_out,
+                       bias_dev ? bias : (bias_bytes ? h->stage[3] : nullptr), dO + h0 * head_out,
                        row_max ? reinterpret_cast<float*>(dM + h0 * head_row) : nullptr,
                        row_sum ? reinterpret_cast<float*>(dL + h0 * head_row) : nullptr,
                        static_cast<char*>(h->stage[7]) + (size_t)c * Lc.total, h->tickets + 2 * h0, h->stream, false);

@@ -91,3 +91,15 @@ def test_out_dtype_validation(ba):
         ba.forward(Q, K, V, out_dtype=torch.float16)
     with pytest.raises(pkg.ShapeError):
         ba.forward(Q, K, V, out=torch.empty(1, 1, 64, 32, device="cuda"), out_dtype=torch.bfloat16)
+
+
+def test_host_entry_point_with_the_bias_resident_on_the_device(ba):
+    """ba_params.bias_on_device: Q, K, V, O are host buffers, the bias table already lives on the GPU -- same bits as the call
+    that copies the table from host memory."""
+    Q, K, V, bias = _inputs(3, 4, 197, 64)
+    hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
+    a = ba.forward_host(hQ, hK, hV, bias.contiguous().cpu())
+    b = ba.forward_host(hQ, hK, hV, bias)            # strided device view (row stride 200)
+    c = ba.forward_host(hQ, hK, hV, bias.contiguous())
+    assert torch.equal(a, b) and torch.equal(a, c)
+    assert torch.equal(a, ba.forward(Q, K, V, bias).cpu())
