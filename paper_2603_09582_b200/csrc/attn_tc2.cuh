@@ -169,6 +169,11 @@ __device__ __forceinline__ void sts_u32_volatile(uint32_t addr, uint32_t v) {
 #else
 #define BA_STAMP3() do { } while (0)
 #endif
+#ifdef BA_DEV_TL_EPI  // dev builds only: stamps around the epilogue's phases (scripts/timeline_units.py ... epi)
+#define BA_STAMP4() BA_STAMP2()
+#else
+#define BA_STAMP4() do { } while (0)
+#endif
 #define BA_STAMP2()                                                      \
     do {                                                                 \
         if (TL && tl_buf && tl_n < kTlStamps) tl_buf[tl_n++] = clock64(); \
@@ -700,11 +705,14 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                 warp_arrive(&sm->pfull[X][st], (int)(lane0 ^ 1u));
             }
             // ---------------------------------------------------------------- epilogue: O / l for my half of the columns
+            BA_STAMP4();
             mbar_wait(&sm->pvdone[X][(gx - 1) & 1u], ((gx - 1) >> 1) & 1u);
+            BA_STAMP4();
             tc_fence_after();
             sm->xch[X][half][r] = l0 + l1;
             pair_sync(pair_id);
             const float l = (l0 + l1) + sm->xch[X][half ^ 1][r];
+            BA_STAMP4();
             const float inv_l = I8 ? 1.0f / l / 255.0f : 1.0f / l;
             const int vc0 = I8 ? prm.vcol0 : 0, dcols = I8 ? prm.dsl : d;  // I8: this pass owns O columns [vc0, vc0 + dcols)
             float* orow = a.O + ((int64_t)head * N + row) * d + vc0;
@@ -765,6 +773,7 @@ attn_tc2_kernel(const __grid_constant__ Params2 prm, const __grid_constant__ CUt
                     }
                 }
             }
+            BA_STAMP4();
             tc_fence_before();
             if (stats && half == 0 && row < N) {
                 if (a.row_max) a.row_max[(int64_t)head * N + row] = (I8 ? m_run : m_true) * kLn2;
