@@ -102,6 +102,11 @@ static int launch_tc2_any(const FwdArgs& a, const int8_t* vq, int ldq, int vcol0
     if (smem_bytes2(prm, kpad) > kSmemMax2) prm.vst = 3;
     if (smem_bytes2(prm, kpad) > kSmemMax2 && prm.bst > 4) prm.bst = 4;
     if (smem_bytes2(prm, kpad) > kSmemMax2) return 0;
+    // dev knobs: shallower rings than the shared memory allows (to reproduce one shape's ring depths on another)
+    if (env_long("BA_QST", 0) > 0) prm.qst = (int)std::min<long>(prm.qst, env_long("BA_QST", 0));
+    if (env_long("BA_KST", 0) > 0) prm.kst = (int)std::min<long>(prm.kst, env_long("BA_KST", 0));
+    if (env_long("BA_VST", 0) > 0) prm.vst = (int)std::min<long>(prm.vst, env_long("BA_VST", 0));
+    if (env_long("BA_BST", 0) > 0) prm.bst = (int)std::min<long>(prm.bst, env_long("BA_BST", 0));
 
     CUtensorMap vmap, bmap, omap;
     const cuuint32_t estr[3] = {1, 1, 1};
