@@ -395,7 +395,8 @@ class BinaryAttention:
                                                 _ptr(m), _ptr(l), None, self._stream()))
         return (O, m, l) if return_stats else O
 
-    def forward_host(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None, out_dtype=torch.float32):
+    def forward_host(self, Q, K, V, bias=None, scale=None, kernel="auto", out=None, out_dtype=torch.float32, quantize_pv=False,
+                     block_cols=None):
         """Same call with HOST tensors (ideally pinned): H2D + kernels + D2H inside ba_binary_attention_host."""
         if Q.is_cuda or K.is_cuda or V.is_cuda:
             raise ValidationError("forward_host takes CPU tensors")
@@ -406,7 +407,7 @@ class BinaryAttention:
         bias, bias_t = self._check_bias(bias, H, N)
         if bias_t is not None and not isinstance(bias, (Relative1dBias, Relative2dBias)) and not bias_t.is_cuda:
             bias = bias_t = bias_t.contiguous()
-        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel)
+        p = self._params(B, H, N, d, Q.dtype, bias, scale, kernel, quantize_pv, block_cols)
         p.bias_on_device = 1 if (bias_t is not None and bias_t.is_cuda) else 0  # a table that already lives on the GPU (a model parameter)
         if out_dtype not in (torch.float32, torch.bfloat16):
             raise ValidationError("out_dtype must be torch.float32 or torch.bfloat16")

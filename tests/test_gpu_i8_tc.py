@@ -123,3 +123,23 @@ def test_tensor_core_int8_pv_long_sequence_sample(ba, port):
     O = ba.forward(Q, K, V, quantize_pv=True, kernel="tcgen05")[0, 0].cpu().numpy().astype(np.float64)
     y8 = port.binary_attention_fused(q, k, v, quantize_pv=True, block_cols=64)[0]
     assert np.abs(O - y8).max() <= 1e-3, np.abs(O - y8).max()
+
+
+def test_tensor_core_int8_pv_through_the_host_entry_point(ba):
+    """ba_binary_attention_host with quantize_pv = 1: the head grid flows through the chunked H2D / kernel / D2H pipeline, every
+    chunk with its own workspace slice (packed planes, s8 levels, scales, expanded planes) -- same bits as the device call.
+    (A host bias table with 394-byte rows is not TMA-able: that call takes the CUDA-core kernel in auto mode and refuses
+    kernel="tcgen05"; a table with 16-byte rows -- here the device-resident one, row stride 200 -- stays on the tensor cores.)"""
+    import torch
+    import paper_2603_09582_b200 as pkg
+    g = torch.Generator(device="cuda").manual_seed(9)
+    Q, K, V = (torch.randn(40, 12, 197, 64, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    bias = (0.5 * torch.randn(12, 197, 200, device="cuda", generator=g)).to(torch.bfloat16)[:, :, :197]
+    hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
+    assert torch.equal(ba.forward_host(hQ, hK, hV, quantize_pv=True, kernel="tcgen05"), ba.forward(Q, K, V, quantize_pv=True, kernel="tcgen05").cpu())
+    ref = ba.forward(Q, K, V, bias, quantize_pv=True, kernel="tcgen05").cpu()
+    assert torch.equal(ba.forward_host(hQ, hK, hV, bias, quantize_pv=True, kernel="tcgen05"), ref)  # bias resident on the device
+    with pytest.raises(pkg.UnsupportedError):
+        ba.forward_host(hQ, hK, hV, bias.contiguous().cpu(), quantize_pv=True, kernel="tcgen05")
+    auto = ba.forward_host(hQ, hK, hV, bias.contiguous().cpu(), quantize_pv=True)  # CUDA-core kernel: within a level flip of the other
+    assert float((auto - ref).abs().max()) <= 1e-3  # 480 heads: a few weights land on the other side of a .5 rounding boundary
