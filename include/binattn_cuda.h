@@ -79,7 +79,8 @@ typedef struct {
     int32_t in_dtype;    /* ba_dtype of Q, K, V */
     int32_t bias_mode;   /* ba_bias_mode */
     int32_t bias_heads;  /* 1 or H */
-    int32_t bias_dtype;  /* BA_BF16 or BA_F32 */
+    int32_t bias_dtype;  /* BA_BF16 or BA_F32 (bf16 tables take the TMA path of the tensor-core kernels; rows that are not
+                            16-byte multiples are re-laid once per call into a padded copy owned by the handle) */
     int64_t bias_ld;     /* elements; 0 -> N */
     float inv_tau;       /* 1 / temperature; must be > 0 (attention.cpp:24-25); use 1/sqrt(d) for AttentionConfig::make */
     int32_t kernel;      /* ba_kernel */

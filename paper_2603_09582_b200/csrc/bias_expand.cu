@@ -26,4 +26,32 @@ int launch_expand_rel2d(const void* tables, int dtype, int heads, int N, int g, 
     return e == cudaSuccess ? 1 : -(int)e;
 }
 
+// Dense bf16 table whose rows are not 16-byte multiples (a contiguous [H,N,N] table with N % 8 != 0 -- the natural layout of the
+// N = 197 ViT configs) -> the same table with rows padded to ld_out = 8-element multiples, which the TMA tile loads need.  The
+// direct-load bias path the unpadded table would take is 2x slower at N = 197 (0.165 -> 0.335 ms) and costs the integer P.V
+// mode its tensor-core kernel altogether (0.36 -> 3.05 ms); the copy is ~1 MB there.  One thread per 8 output elements.
+__global__ void __launch_bounds__(256) pad_bias_rows_kernel(const uint16_t* __restrict__ in, int64_t ld_in, int N, int64_t ld_out,
+                                                            uint16_t* __restrict__ out, int64_t rows) {
+    const int cpr = (int)(ld_out / 8);  // 16-byte chunks per output row
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * cpr) return;
+    const int64_t row = idx / cpr;
+    const int c0 = (int)(idx - row * cpr) * 8;
+    const uint16_t* src = in + row * ld_in + c0;
+    uint16_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = c0 + i < N ? src[i] : (uint16_t)0;
+    *reinterpret_cast<uint4*>(out + row * ld_out + c0) = *reinterpret_cast<const uint4*>(v);
+}
+
+// in: [heads, N, ld_in] bf16 (ld_in >= N), out: [heads, N, ld_out] with ld_out % 8 == 0; out must be 16-byte aligned.
+int launch_pad_bias_rows(const void* in, int64_t ld_in, int heads, int N, int64_t ld_out, void* out, cudaStream_t stream) {
+    const int64_t rows = (int64_t)heads * N, chunks = rows * (ld_out / 8);
+    if (chunks == 0) return 0;
+    pad_bias_rows_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(static_cast<const uint16_t*>(in), ld_in, N, ld_out,
+                                                                            static_cast<uint16_t*>(out), rows);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -(int)e;
+}
+
 }  // namespace ba

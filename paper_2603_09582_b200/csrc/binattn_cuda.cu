@@ -16,6 +16,7 @@
 
 namespace ba {
 int launch_expand_rel2d(const void* tables, int dtype, int heads, int N, int g, float* out, cudaStream_t stream);  // bias_expand.cu
+int launch_pad_bias_rows(const void* in, int64_t ld_in, int heads, int N, int64_t ld_out, void* out, cudaStream_t stream);  // bias_expand.cu
 int launch_pack_signs_qk(const void* Q, const void* K, int in_dtype, int64_t heads, int N, int d, uint64_t* q_words,
                          uint64_t* k_words, float* mu_q, float* mu_k, float* partials, unsigned int* tickets,
                          cudaStream_t stream);
@@ -150,6 +151,8 @@ struct ba_handle {
     size_t diag_bytes = 0;
     void* rel2d = nullptr;      // Relative2dBias expanded to a dense fp32 [bias_heads, N, N] table (shapes the in-kernel path does not take)
     size_t rel2d_bytes = 0;
+    void* bias_pad = nullptr;   // dense bf16 bias re-laid with 16-byte rows for the TMA tile loads (tables whose rows are not)
+    size_t bias_pad_bytes = 0;
     // host-buffer path: copy-in stream, compute stream, copy-out stream + per-chunk events
     cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
     cudaEvent_t ev_in[kHostChunksMax] = {}, ev_done[kHostChunksMax] = {};
@@ -256,6 +259,7 @@ int ba_destroy(ba_handle* h) {
     if (h->partials) cudaFree(h->partials);
     if (h->diag) cudaFree(h->diag);
     if (h->rel2d) cudaFree(h->rel2d);
+    if (h->bias_pad) cudaFree(h->bias_pad);
     for (void* s : h->stage)
         if (s) cudaFree(s);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -482,6 +486,29 @@ int ba_attention_fidelity_host(ba_handle* h, const double* p_ref, const double* 
     return rc;
 }
 
+// A dense bf16 bias table the tensor-core kernels cannot tile by TMA (rows or base not 16-byte aligned: e.g. a contiguous
+// [H,197,197] table) is copied once per call into a row-padded table owned by the handle; *bias and *pp (a copy of the
+// caller's params with the new row stride) then describe that table.  Tables above 2 GiB are left alone (they take the
+// direct-load path of the first-generation kernel / the CUDA-core kernel of the integer mode).
+static int maybe_pad_bias(ba_handle* h, const ba_params* p, int kernel, const void** bias, ba_params* pp, cudaStream_t stream) {
+    *pp = *p;
+    if (p->bias_mode != BA_BIAS_DENSE || !*bias || p->bias_dtype != BA_BF16 || p->in_dtype != BA_BF16 || kernel != BA_KERNEL_TCGEN05)
+        return BA_OK;
+    const int64_t ld = p->bias_ld ? p->bias_ld : p->N;
+    if ((ld * 2) % 16 == 0 && reinterpret_cast<uintptr_t>(*bias) % 16 == 0) return BA_OK;
+    const int64_t ld_out = ((int64_t)p->N + 7) / 8 * 8;
+    const size_t need = (size_t)p->bias_heads * p->N * ld_out * 2;
+    if (need > ((size_t)2 << 30) || getenv("BA_NO_BIAS_PAD")) return BA_OK;
+    int rc = ensure(&h->bias_pad, &h->bias_pad_bytes, need, false);
+    if (rc) return rc;
+    const int n = ba::launch_pad_bias_rows(*bias, ld, p->bias_heads, p->N, ld_out, h->bias_pad, stream);
+    if (n < 0) return fail(BA_ERR_CUDA, "bias row padding launch: %s", cudaGetErrorString((cudaError_t)(-n)));
+    h->launches += n;
+    *bias = h->bias_pad;
+    pp->bias_ld = ld_out;
+    return BA_OK;
+}
+
 // One K1 + K2 pass over `heads` consecutive heads starting at grid index head0; every tensor pointer already points at
 // that first head.  `ws` holds make_layout(p, heads).total bytes, `tickets` 2*heads zeroed counters.
 static int fwd_range(ba_handle* h, const ba_params* p, int kernel, int64_t head0, int64_t heads, const void* Q, const void* K,
@@ -603,6 +630,9 @@ int ba_binary_attention_fwd(ba_handle* h, const ba_params* p, const void* Q, con
     BA_BIND_DEVICE(h);
     int kernel = 0;
     if ((rc = resolve_kernel(p, &kernel))) return rc;
+    ba_params padded_params;
+    if ((rc = maybe_pad_bias(h, p, kernel, &bias, &padded_params, stream))) return rc;
+    p = &padded_params;
     const Layout L = make_layout(p);
     if (!workspace) {
         if ((rc = ensure(&h->ws, &h->ws_bytes, L.total, false))) return rc;
@@ -703,6 +733,12 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
     char* const dM = static_cast<char*>(h->stage[5]);
     char* const dL = static_cast<char*>(h->stage[6]);
     if (bias_bytes && !bias_dev) BA_CUDA(cudaMemcpyAsync(h->stage[3], bias, bias_bytes, cudaMemcpyHostToDevice, h->stream_in));
+    // the table on the device, once per call (re-laid with 16-byte rows when the TMA tile loads need that), on the copy stream:
+    // every chunk's kernels wait for an event recorded on it after this point
+    const void* dbias = bias_dev ? bias : (bias_bytes ? h->stage[3] : nullptr);
+    ba_params padded_params;
+    if ((rc = maybe_pad_bias(h, p, kernel, &dbias, &padded_params, h->stream_in))) return rc;
+    p = &padded_params;
     size_t h0 = 0;
     for (int c = 0; c < chunks; h0 += plan[c], ++c) {
         const size_t nh = plan[c];
@@ -715,7 +751,7 @@ int ba_binary_attention_host(ba_handle* h, const ba_params* p, const void* Q, co
         BA_CUDA(cudaEventRecord(h->ev_in[c], h->stream_in));
         BA_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
         rc = fwd_range(h, p, kernel, (int64_t)h0, (int64_t)nh, dQ + h0 * head_in, dK + h0 * head_in, dV + h0 * head_in,
-                       bias_dev ? bias : (bias_bytes ? h->stage[3] : nullptr), dO + h0 * head_out,
+                       dbias, dO + h0 * head_out,
                        row_max ? reinterpret_cast<float*>(dM + h0 * head_row) : nullptr,
                        row_sum ? reinterpret_cast<float*>(dL + h0 * head_row) : nullptr,
                        static_cast<char*>(h->stage[7]) + (size_t)c * Lc.total, h->tickets + 2 * h0, h->stream, false);

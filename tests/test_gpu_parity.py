@@ -618,3 +618,27 @@ def test_full_size_c5_properties(ba, port, with_rel1d):
         perm = torch.randperm(n, device="cuda", generator=g)
         Op = ba.forward(Q[:, :2], K[:, :2][:, :, perm], V[:, :2][:, :, perm])
         assert (Op - O[:, :2]).abs().max().item() <= TOL_O
+
+
+@pytest.mark.parametrize("n,d", [(197, 64), (577, 64), (2049, 64), (130, 128)])
+def test_contiguous_bias_table_with_unaligned_rows(ba, n, d):
+    """A contiguous [H,N,N] bf16 table with N % 8 != 0 (rows that are not 16-byte multiples: what a caller of the reference
+    naturally holds for N = 197) is re-laid with padded rows once per call and takes the same TMA path as a padded table: the
+    two give the same bits, in the bf16 mode and in the integer mode; BA_NO_BIAS_PAD=1 keeps the direct-load path alive."""
+    import os
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(13)
+    Q, K, V = (torch.randn(2, 3, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    padded = (0.5 * torch.randn(3, n, (n + 7) // 8 * 8, device="cuda", generator=g)).to(torch.bfloat16)[:, :, :n]
+    contig = padded.contiguous()
+    assert contig.stride(1) == n and padded.stride(1) != n
+    a = ba.forward(Q, K, V, padded)
+    assert torch.equal(ba.forward(Q, K, V, contig), a)
+    assert torch.equal(ba.forward(Q, K, V, contig[:1]), ba.forward(Q, K, V, padded[:1]))  # one shared table
+    assert torch.equal(ba.forward(Q, K, V, contig, quantize_pv=True), ba.forward(Q, K, V, padded, quantize_pv=True))
+    os.environ["BA_NO_BIAS_PAD"] = "1"
+    try:
+        slow = ba.forward(Q, K, V, contig)
+    finally:
+        del os.environ["BA_NO_BIAS_PAD"]
+    assert float((slow - a).abs().max()) <= 2e-3  # the direct-load path (first-generation kernel for every N): same math, other tiling
