@@ -298,6 +298,61 @@ __global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_kernel(const __g
     finish_head_sum(((dacc[0] + dacc[1]) + (dacc[2] + dacc[3])) * 0.125f, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
 }
 
+// bf16 rows whose vector count is not a power of two (VPR 16-byte vectors per row, 8 < VPR < 16: d = 72 has 9): the lane-slot
+// mapping of pack_signs_bf16_kernel<16> leaves 7 of every 16 lanes idle there (K1 at 0.41-0.49 of HBM on the d = 72 configs).
+// A chunk of rows is a CONTIGUOUS array of vectors, so here lane slot i simply loads vector i of the chunk; (row, vector) =
+// (i / VPR, i % VPR) with a compile-time divisor.  Every lane owns one byte of the packed row; the lane of vector 8 writes
+// bytes 8..15 of the row as one u64 (its byte, then the zero pad bits -- tensor.hpp:57-94).
+template <int VPR>
+__global__ void __launch_bounds__(kPackThreads) pack_signs_bf16_odd_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int chunks) {
+    static_assert(VPR == 9, "the pad store below assumes the last vector of a row sits at byte 8");
+    asm volatile("griddepcontrol.launch_dependents;");   // see pack_signs_bf16_kernel
+    constexpr int kU = 9;                                // loads in flight per lane; 2 x 9 x 128 slots = 256 rows x 9 vectors
+    const PackJob& job = jobs.job[blockIdx.z];
+    const int head = blockIdx.x, chunk = blockIdx.y;
+    const int row0 = chunk * kPackRowsPerCta;
+    const int rows = min(kPackRowsPerCta, N - row0);
+    const int slots = rows * VPR;
+    const char* xbase = static_cast<const char*>(job.X) + ((int64_t)head * N + row0) * d * 2;
+    unsigned char* wbytes = reinterpret_cast<unsigned char*>(job.words + ((int64_t)head * N + row0) * 2);
+    float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int p0 = 0; p0 < 2; ++p0) {
+        if (p0 * kU * kPackThreads >= slots) break;      // block-uniform
+        uint4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = (p0 * kU + u) * kPackThreads + threadIdx.x;
+            v[u] = ldg_nc_16_pred(xbase + (uint32_t)i * 16u, i < slots);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = (p0 * kU + u) * kPackThreads + threadIdx.x;
+            if ((p0 * kU + u) * kPackThreads >= slots) break;  // block-uniform
+            const uint32_t r[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            uint32_t neg[4], mag[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                mag[k] = r[k] & 0x7FFF7FFFu;
+                neg[k] = ((r[k] & (mag[k] + 0x7FFF7FFFu)) | (mag[k] + 0x007F007Fu)) & 0x80008000u;  // see bf16x8_signs_abs
+            }
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%8}, {%0,%1,%2,%3};"
+                : "+f"(dacc[0]), "+f"(dacc[1]), "+f"(dacc[2]), "+f"(dacc[3])
+                : "r"(mag[0]), "r"(mag[1]), "r"(mag[2]), "r"(mag[3]), "r"(0x3F803F80u));
+            const uint32_t lo = __byte_perm(neg[0], neg[1], 0x7531), hi = __byte_perm(neg[2], neg[3], 0x7531);
+            const uint32_t nbits = (((lo >> 7) * 0x01020408u) >> 24) | ((((hi >> 7) * 0x01020408u) >> 24) << 4);
+            const uint32_t byte = ~nbits & 0xFFu;
+            if (i < slots) {
+                const int row = i / VPR, vs = i - row * VPR;
+                if (vs == 8) *reinterpret_cast<uint64_t*>(wbytes + row * 16 + 8) = (uint64_t)byte;
+                else wbytes[row * 16 + vs] = (unsigned char)byte;
+            }
+        }
+    }
+    finish_head_sum(((dacc[0] + dacc[1]) + (dacc[2] + dacc[3])) * 0.125f, job, head, chunk, chunks, 1.0 / ((double)N * (double)d));
+}
+
 // Generic path: any d, any alignment; one thread per (row, u64 word), scalar loads.
 __global__ void __launch_bounds__(kPackThreads) pack_signs_generic_kernel(const __grid_constant__ PackJobs jobs, int N, int d, int dtype,
                                                                           int chunks) {
@@ -335,6 +390,8 @@ static int launch_pack_jobs(const PackJobs& jobs, int njobs, int in_dtype, int64
     for (int j = 0; j < njobs; ++j) vec = vec && (reinterpret_cast<uintptr_t>(jobs.job[j].X) % 16 == 0);
     if (vec && in_dtype == BA_BF16 && d == 64)
         pack_signs_bf16_kernel<8><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
+    else if (vec && in_dtype == BA_BF16 && d == 72 && !getenv("BA_PACK_NO_D72"))
+        pack_signs_bf16_odd_kernel<9><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
     else if (vec && in_dtype == BA_BF16 && d > 64 && d <= 128)
         pack_signs_bf16_kernel<16><<<grid, kPackThreads, 0, stream>>>(jobs, N, d, chunks);
     else if (vec && in_dtype == BA_BF16)
