@@ -61,7 +61,13 @@ constexpr int kBSub = 16384;       // one bias tile: 128 rows x 64 columns bf16,
 #endif
 constexpr float kThr2 = BA_THR2;     // lazy-rescale threshold, log2 units
 constexpr float kFastBound = 32.0f;  // FAST path when d * mu_q mu_k / tau * log2(e) <= this (weights stay >= 2^-64)
-constexpr int kRegsSoftmax2 = 104, kRegsCtrl2 = 64;  // the pool is what the launch allocated: 640 x 96 = 512 x 104 + 128 x 64
+#ifndef BA_REGS_SOFTMAX
+#define BA_REGS_SOFTMAX 104  // dev knobs (setmaxnreg targets); the defaults are the whole launch allocation
+#endif
+#ifndef BA_REGS_CTRL
+#define BA_REGS_CTRL 64
+#endif
+constexpr int kRegsSoftmax2 = BA_REGS_SOFTMAX, kRegsCtrl2 = BA_REGS_CTRL;  // the pool is what the launch allocated: 640 x 96 = 512 x 104 + 128 x 64
 
 struct Smem2 {
     uint64_t qfull[2], qfree[2];  // Q tiles of a unit expanded / every S MMA of the unit retired
