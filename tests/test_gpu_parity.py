@@ -460,6 +460,12 @@ def test_torch_library_op(ba, port):
         fq = torch.empty(1, 2, n, d, dtype=torch.bfloat16, device="cuda")
         out = torch.ops.binattn.binary_attention(fq, fq, fq, None, None)
         assert out.shape == (1, 2, n, d) and out.dtype == torch.float32
+        out = torch.ops.binattn.binary_attention_ex(fq, fq, fq, None, None, True, True)
+        assert out.shape == (1, 2, n, d) and out.dtype == torch.bfloat16
+    # the extended op: the reference's default integer P.V arithmetic and / or bfloat16 output
+    assert torch.equal(torch.ops.binattn.binary_attention_ex(Q, K, V, bias, None, True, False), ba.forward(Q, K, V, bias, quantize_pv=True))
+    assert torch.equal(torch.ops.binattn.binary_attention_ex(Q, K, V, bias, None, False, True),
+                       ba.forward(Q, K, V, bias).to(torch.bfloat16))
 
 
 def test_packed_planes_as_batf_files(ba, port, tmp_path):
