@@ -330,12 +330,25 @@ int ba_shard_units(const ba_params* p, int world, int rank, int64_t* begin, int6
     return ba_shard_range((int64_t)p->B * p->H * ba::units_per_head(p->N), world, rank, begin, end);
 }
 
+// Heads with fewer keys than this run the CUDA-core kernel under BA_KERNEL_AUTO: a 64-key tensor-core tile has nothing to win
+// there, and with a handful of keys every row is peaked, which is where the bf16 weights of the tensor-core path cost accuracy
+// (2.1e-3 ... 2.5e-3 at N = 2 and 7 in scripts/fuzz_auto.py; the CUDA-core kernel keeps fp32 weights).  BA_KERNEL_TCGEN05 still
+// takes them.
+static const int kAutoMinKeysTc = 32;
+
 int ba_select_kernel(const ba_params* p) {
     if (check_params(p, true) != BA_OK) return -1;
-    if (p->quantize_pv) return p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT;
     const char* why = nullptr;
     if (p->kernel == BA_KERNEL_SIMT) return BA_KERNEL_SIMT;
-    return ba::tcgen05_supported(p, &why) ? BA_KERNEL_TCGEN05 : (p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT);
+    if (p->quantize_pv) {  // the tensor-core kernel of the integer mode where the launch will take it (see ba_params.quantize_pv)
+        const int bc = p->block_cols ? p->block_cols : (p->N < 64 ? p->N : 64);
+        const int64_t ld = p->bias_ld ? p->bias_ld : p->N;
+        const bool bias_ok = p->bias_mode == BA_BIAS_NONE || (p->bias_mode == BA_BIAS_DENSE && p->bias_dtype == BA_BF16 && ld >= p->N);
+        const bool tc = ba::tcgen05_supported(p, &why) && ba::tc2_i8_shape_ok(p->in_dtype, p->N, p->d) && bc == 64 && bias_ok;
+        return tc ? BA_KERNEL_TCGEN05 : (p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT);
+    }
+    if (!ba::tcgen05_supported(p, &why)) return p->kernel == BA_KERNEL_TCGEN05 ? -1 : BA_KERNEL_SIMT;
+    return (p->kernel == BA_KERNEL_AUTO && p->N < kAutoMinKeysTc) ? BA_KERNEL_SIMT : BA_KERNEL_TCGEN05;
 }
 
 int ba_pack_signs(ba_handle* h, const ba_params* p, const void* X, uint64_t* words, float* mu, void* stream) {
@@ -607,7 +620,7 @@ static int resolve_kernel(const ba_params* p, int* kernel) {
             return fail(BA_ERR_UNSUPPORTED, "quantize_pv=1 on the tensor cores needs bf16 inputs, d %% 8 == 0, d <= 128 and N >= 128");
         return BA_OK;
     }
-    if (k == BA_KERNEL_AUTO) k = tc_ok ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
+    if (k == BA_KERNEL_AUTO) k = (tc_ok && p->N >= kAutoMinKeysTc) ? BA_KERNEL_TCGEN05 : BA_KERNEL_SIMT;
     if (k == BA_KERNEL_TCGEN05 && !tc_ok) return fail(BA_ERR_UNSUPPORTED, "tcgen05 kernel: %s", why);
     if (k != BA_KERNEL_TCGEN05 && k != BA_KERNEL_SIMT) return fail(BA_ERR_VALIDATION, "unknown kernel id");
     *kernel = k;
